@@ -1,0 +1,509 @@
+// dfftb executor: contexts (make_context, plan.hpp:359-390), lowering of a
+// plan to fused GPU passes + group barriers, and execute (plan.hpp:463-535).
+//
+// Lowering.  The reference runs, per rank, LocalFftStage -> TransposeStage
+// (pack, all_to_all, unpack; exchange.hpp:547-590) [-> LocalTransposeStage]
+// ... -> NormalizeStage.  Here every FFT stage becomes ONE kernel launch
+// whose store epilogue writes each output element to its final address in
+// the stage's target layout:
+//   FFT followed by a transpose  -> peer exchange buffers of the grid-axis
+//                                   group (NVLink stores), then a barrier
+//   FFT followed by Normalize    -> user output, scaled by 1/N
+//   last FFT                     -> user output
+//   FFT followed by a local FFT  -> private work buffer
+// so each axis costs one read + one write of the local block.
+#include <cuda_runtime.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "exec.hpp"
+#include "kernels.hpp"
+
+namespace dfftb {
+
+#define CUDA_TRY(x)                                                              \
+  do {                                                                           \
+    cudaError_t e_ = (x);                                                        \
+    if (e_ != cudaSuccess)                                                       \
+      raise(DFFTB_CudaError, std::string(#x) + ": " + cudaGetErrorString(e_));    \
+  } while (0)
+
+static constexpr uint64_t kHandleMagic = 0x64666674625f3031ull;  // "dfftb_01"
+static constexpr size_t kFlagsBytes = 4096;
+static constexpr unsigned long long kBarrierTimeoutNs = 60ull * 1000 * 1000 * 1000;
+
+void* Ctx::exch(int r, int slot, int parity) const {
+  char* base = static_cast<char*>(peer_region[r]);
+  return base + flags_bytes + (size_t)(2 * slot + parity) * exch_bytes;
+}
+
+uint64_t* Ctx::flags_of(int r) const { return static_cast<uint64_t*>(peer_region[r]); }
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+// Bytes of the largest complex block any rank holds in any layout of the
+// plan family (forward and backward of the same geometry), so one context
+// serves execute(bwd, execute(fwd, x, ctx), ctx) as in test_plan.cpp:116-133.
+static size_t family_bytes(const Plan& plan) {
+  dfftb_plan_options o = plan.options;
+  const int kf = plan.kind == DFFTB_C2C ? DFFTB_C2C : DFFTB_R2C;
+  const int kb = plan.kind == DFFTB_C2C ? DFFTB_C2C : DFFTB_C2R;
+  int64_t m = 1;
+  for (int d = 0; d < 2; ++d) {
+    Plan p = build_plan(plan.dims, plan.decomp, plan.grid, d == 0 ? kf : kb, d, plan.prec, o);
+    for (const auto& st : p.stages) {
+      if (st.type == StageType::Normalize) continue;
+      m = std::max(m, st.before.max_local_count());
+      if (st.type != StageType::LocalTranspose || true) m = std::max(m, st.after.max_local_count());
+    }
+  }
+  return (size_t)m * 2 * plan.prec;
+}
+
+static void check_lengths(const Plan& plan) {
+  if (plan.dims.size() != 3 && plan.dims.size() != 2)
+    raise(DFFTB_Unsupported, "the B200 path executes 2-D and 3-D transforms");
+  for (auto n : plan.dims)
+    if (!pass_length_supported(n))
+      raise(DFFTB_Unsupported, "axis length " + std::to_string(n) +
+                                   " not supported on the B200 path (powers of two <= 4096)");
+  for (int g : plan.grid)
+    if (g > kMaxDest) raise(DFFTB_Unsupported, "grid factors above 8 are not supported");
+}
+
+Ctx* ctx_create(const Plan& plan, int rank, int device) {
+  if (rank < 0 || rank >= plan.nranks()) raise(DFFTB_InvalidRank, "rank out of range");
+  check_lengths(plan);
+  DeviceGuard g(device);
+  CUDA_TRY(cudaSetDevice(device));
+  auto ctx = std::make_unique<Ctx>();
+  ctx->rank = rank;
+  ctx->nranks = plan.nranks();
+  ctx->device = device;
+  ctx->prec = plan.prec;
+  ctx->dims = plan.dims;
+  ctx->grid = plan.grid;
+  ctx->decomp = plan.decomp;
+  ctx->kind_family = plan.kind == DFFTB_C2C ? 0 : 1;
+  const size_t blk = (family_bytes(plan) + 255) / 256 * 256;
+  ctx->flags_bytes = kFlagsBytes;
+  ctx->exch_bytes = blk;
+  ctx->region_bytes = kFlagsBytes + 4 * blk;
+  ctx->work_bytes = blk;
+  CUDA_TRY(cudaMalloc(&ctx->region, ctx->region_bytes));
+  CUDA_TRY(cudaMemset(ctx->region, 0, kFlagsBytes));
+  CUDA_TRY(cudaMalloc(&ctx->work, ctx->work_bytes));
+  CUDA_TRY(cudaMalloc(&ctx->dstat, 8 * sizeof(unsigned long long)));
+  CUDA_TRY(cudaMemset(ctx->dstat, 0, 8 * sizeof(unsigned long long)));
+  // twiddle tables w[m] = exp(-2 pi i m / n) in double, cast to T
+  // (TwiddleTable, kernels.hpp:66-98); forward only: backward is conj(F(conj x))
+  for (auto n64 : plan.dims) {
+    const int n = (int)n64;
+    if (ctx->twiddles.count(n)) continue;
+    std::vector<double> wd(2 * n);
+    std::vector<float> wf(2 * n);
+    for (int m = 0; m < n; ++m) {
+      const double a = -2.0 * M_PI * (double)m / (double)n;
+      wd[2 * m] = std::cos(a);
+      wd[2 * m + 1] = std::sin(a);
+      wf[2 * m] = (float)wd[2 * m];
+      wf[2 * m + 1] = (float)wd[2 * m + 1];
+    }
+    void* d = nullptr;
+    CUDA_TRY(cudaMalloc(&d, 2 * n * plan.prec));
+    CUDA_TRY(cudaMemcpy(d, plan.prec == 8 ? (void*)wd.data() : (void*)wf.data(), 2 * n * plan.prec,
+                        cudaMemcpyHostToDevice));
+    ctx->twiddles[n] = d;
+  }
+  ctx->peer_region.assign(ctx->nranks, nullptr);
+  ctx->peer_opened.assign(ctx->nranks, false);
+  ctx->peer_region[rank] = ctx->region;
+  if (ctx->nranks == 1) ctx->connected = true;
+  return ctx.release();
+}
+
+void ctx_export(const Ctx& ctx, CtxHandle* h) {
+  std::memset(h, 0, sizeof(*h));
+  DeviceGuard g(ctx.device);
+  cudaIpcMemHandle_t ih;
+  CUDA_TRY(cudaIpcGetMemHandle(&ih, ctx.region));
+  std::memcpy(h->ipc, &ih, sizeof(ih));
+  h->pid = (int64_t)getpid();
+  h->device = ctx.device;
+  h->dptr = (uint64_t)(uintptr_t)ctx.region;
+  h->bytes = ctx.region_bytes;
+  h->magic = kHandleMagic;
+}
+
+void ctx_connect(Ctx& ctx, const CtxHandle* handles) {
+  DeviceGuard g(ctx.device);
+  for (int r = 0; r < ctx.nranks; ++r) {
+    const CtxHandle& h = handles[r];
+    if (h.magic != kHandleMagic) raise(DFFTB_BadMagic, "context handle has a bad magic");
+    if (h.bytes != ctx.region_bytes) raise(DFFTB_CountMismatch, "peer context sizes differ");
+    if (r == ctx.rank) continue;
+    if (h.pid == (int64_t)getpid()) {
+      // same process (thread-per-GPU world): direct peer pointer
+      if (h.device != ctx.device) {
+        int can = 0;
+        CUDA_TRY(cudaDeviceCanAccessPeer(&can, ctx.device, (int)h.device));
+        if (!can) raise(DFFTB_Unsupported, "no peer access between devices");
+        cudaError_t e = cudaDeviceEnablePeerAccess((int)h.device, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+          raise(DFFTB_CudaError, cudaGetErrorString(e));
+        cudaGetLastError();
+      }
+      ctx.peer_region[r] = (void*)(uintptr_t)h.dptr;
+    } else {
+      cudaIpcMemHandle_t ih;
+      std::memcpy(&ih, h.ipc, sizeof(ih));
+      void* p = nullptr;
+      CUDA_TRY(cudaIpcOpenMemHandle(&p, ih, cudaIpcMemLazyEnablePeerAccess));
+      ctx.peer_region[r] = p;
+      ctx.peer_opened[r] = true;
+    }
+  }
+  ctx.connected = true;
+}
+
+void ctx_destroy(Ctx* ctx) {
+  if (!ctx) return;
+  {
+    DeviceGuard g(ctx->device);
+    cudaDeviceSynchronize();
+    for (int r = 0; r < ctx->nranks; ++r)
+      if (ctx->peer_opened[r]) cudaIpcCloseMemHandle(ctx->peer_region[r]);
+    for (auto& kv : ctx->twiddles) cudaFree(kv.second);
+    cudaFree(ctx->region);
+    cudaFree(ctx->work);
+    cudaFree(ctx->dstat);
+    cudaGetLastError();
+  }
+  delete ctx;
+}
+
+void world_create(const Plan& plan, int device, Ctx** out) {
+  const int P = plan.nranks();
+  std::vector<Ctx*> ctxs(P, nullptr);
+  try {
+    for (int r = 0; r < P; ++r) ctxs[r] = ctx_create(plan, r, device);
+  } catch (...) {
+    for (auto* c : ctxs) ctx_destroy(c);
+    throw;
+  }
+  for (int r = 0; r < P; ++r) {
+    for (int q = 0; q < P; ++q) ctxs[r]->peer_region[q] = ctxs[q]->region;
+    ctxs[r]->world_mode = true;
+    ctxs[r]->connected = true;
+    out[r] = ctxs[r];
+  }
+}
+
+// ---------------------------------------------------------------- lowering
+
+struct Op {
+  bool barrier = false;
+  PassParams p{};
+  int n = 1;
+  bool adj = false;
+  bool fused = false;
+  int grid_axis = 0;
+  std::vector<int> members;
+};
+
+static void row_major_strides(const int64_t* len, int nd, int64_t* st) {
+  st[nd - 1] = 1;
+  for (int a = nd - 2; a >= 0; --a) st[a] = st[a + 1] * len[a + 1];
+}
+
+static std::vector<int> group_members(const Dist& d, int me, int g) {
+  auto c = d.coords_of(me);
+  std::vector<int> m(d.grid[g]);
+  for (int q = 0; q < d.grid[g]; ++q) {
+    auto cq = c;
+    cq[g] = q;
+    m[q] = d.rank_of(cq);
+  }
+  return m;
+}
+
+static void check_compatible(const Plan& plan, const Ctx& ctx) {
+  if (plan.nranks() != ctx.nranks) raise(DFFTB_GridMismatch, "communicator size must match the grid");
+  if (plan.dims != ctx.dims || plan.grid != ctx.grid || plan.prec != ctx.prec ||
+      plan.decomp != ctx.decomp)
+    raise(DFFTB_GridMismatch, "context was made for a different plan geometry");
+  if (!ctx.connected) raise(DFFTB_ConfigInvalid, "context is not connected to its peers");
+  if (family_bytes(plan) > ctx.exch_bytes)
+    raise(DFFTB_ArenaExhausted, "context buffers are too small for this plan");
+}
+
+// One rank's program: fused passes and barriers.  `peer` supplies the
+// exchange-buffer base of any world rank (its own mapping of the peers).
+static std::vector<Op> lower(const Plan& plan, const Ctx& ctx, const void* d_in, void* d_out,
+                             int parity) {
+  std::vector<Op> prog;
+  const int me = ctx.rank;
+  const void* cur = d_in;
+  int slot = 0;
+  const auto& S = plan.stages;
+  size_t i = 0;
+  while (i < S.size()) {
+    const Stage& st = S[i];
+    if (st.type != StageType::Fft) raise(DFFTB_ConfigInvalid, "unexpected stage order");
+    const Stage* tr = (i + 1 < S.size() && S[i + 1].type == StageType::Transpose) ? &S[i + 1] : nullptr;
+    const Stage* nm = (i + 1 < S.size() && S[i + 1].type == StageType::Normalize) ? &S[i + 1] : nullptr;
+    const bool last_fft = (i + 1 == S.size()) || nm != nullptr;
+
+    const Dist& Lb = st.before;
+    const int nd = Lb.ndim();
+    int64_t offb[kMaxDims], lenb[kMaxDims], sb[kMaxDims];
+    Lb.extents_of(me, offb, lenb);
+    row_major_strides(lenb, nd, sb);
+    const int v = st.axis;
+    int ax_a = -1, ax_b = -1;
+    for (int a = 0; a < nd; ++a) {
+      if (a == v) continue;
+      if (nd == 3 && ax_a < 0) ax_a = a;
+      else ax_b = a;
+    }
+    Op op;
+    PassParams& p = op.p;
+    p.in = cur;
+    p.A = ax_a >= 0 ? (int)lenb[ax_a] : 1;
+    p.B = (int)lenb[ax_b];
+    p.in_sa = ax_a >= 0 ? sb[ax_a] : 0;
+    p.in_sb = sb[ax_b];
+    p.in_si = sb[v];
+    const int n = st.fkind == DFFTB_C2R ? (int)st.after.dims[v] : (int)lenb[v];
+    op.n = n;
+    p.n_out = st.fkind == DFFTB_R2C ? n / 2 + 1 : n;
+    p.in_mode = st.fkind == DFFTB_R2C ? kInReal : (st.fkind == DFFTB_C2R ? kInHermitian : kInComplex);
+    p.out_real = st.fkind == DFFTB_C2R;
+    p.inverse = st.dir == DFFTB_BACKWARD;
+    p.scale = nm ? nm->factor : 1.0;
+    p.tw = ctx.twiddles.at(n);
+    p.herm = ctx.dstat;
+    op.adj = p.in_si != 1;
+    if (lenb[v] == 0 && st.fkind != DFFTB_C2R) p.A = 0;
+
+    if (tr) {
+      const Dist& Lo = tr->after;
+      const int g = tr->grid_axis;
+      const int u = tr->before.axis_of_grid[g];
+      op.fused = true;
+      op.grid_axis = g;
+      op.members = group_members(Lo, me, g);
+      p.ndest = (int)op.members.size();
+      p.oblk = (Lo.dims[v] + Lo.grid[g] - 1) / Lo.grid[g];
+      for (int q = 0; q < p.ndest; ++q) {
+        const int rq = op.members[q];
+        int64_t offo[kMaxDims], leno[kMaxDims], so[kMaxDims];
+        Lo.extents_of(rq, offo, leno);
+        row_major_strides(leno, nd, so);
+        Dest& d = p.dest[q];
+        d.ptr = ctx.exch(rq, slot, parity);
+        d.base = offb[u] * so[u];
+        d.sa = ax_a >= 0 ? so[ax_a] : 0;
+        d.sb = so[ax_b];
+        d.sk = so[v];
+      }
+      prog.push_back(op);
+      Op b;
+      b.barrier = true;
+      b.grid_axis = g;
+      b.members = op.members;
+      if (b.members.size() > 1) prog.push_back(b);
+      cur = ctx.exch(me, slot, parity);
+      ++slot;
+      i += tr->transposed ? 3 : 2;  // the LocalTransposeStage is folded in
+    } else {
+      const Dist& Lo = st.after;
+      int64_t offo[kMaxDims], leno[kMaxDims], so[kMaxDims];
+      Lo.extents_of(me, offo, leno);
+      row_major_strides(leno, nd, so);
+      void* out = last_fft ? d_out : ctx.work;
+      p.ndest = 1;
+      p.oblk = p.n_out > 0 ? p.n_out : 1;
+      Dest& d = p.dest[0];
+      d.ptr = out;
+      d.base = 0;
+      d.sa = ax_a >= 0 ? so[ax_a] : 0;
+      d.sb = so[ax_b];
+      d.sk = so[v];
+      prog.push_back(op);
+      cur = out;
+      i += nm ? 2 : 1;
+    }
+  }
+  return prog;
+}
+
+static void launch_op(const Ctx& ctx, const Op& op, uint64_t epoch, cudaStream_t s) {
+  if (op.barrier) {
+    if (ctx.world_mode) return;  // lockstep emulation: stream order is the barrier
+    BarrierParams bp{};
+    bp.nmem = (int)op.members.size();
+    for (int i = 0; i < bp.nmem; ++i) {
+      bp.members[i] = op.members[i];
+      bp.peer_flags[i] = reinterpret_cast<unsigned long long*>(ctx.flags_of(op.members[i]));
+    }
+    bp.me = ctx.rank;
+    bp.my_flags = reinterpret_cast<unsigned long long*>(ctx.flags_of(ctx.rank));
+    bp.epoch = epoch;
+    bp.timeout_ns = kBarrierTimeoutNs;
+    bp.timeout_flag = ctx.dstat + 2;
+    CUDA_TRY(launch_barrier(bp, s));
+    return;
+  }
+  if ((int64_t)op.p.A * op.p.B == 0) return;
+  CUDA_TRY(launch_pass(ctx.prec, op.n, op.p, op.adj, s));
+}
+
+static bool plan_has_c2r(const Plan& plan) {
+  for (const auto& st : plan.stages)
+    if (st.type == StageType::Fft && st.fkind == DFFTB_C2R) return true;
+  return false;
+}
+
+static void validate_finite(const Plan& plan, const Ctx& ctx, const void* d_in, cudaStream_t s) {
+  const int64_t n = plan.input.local_count(ctx.rank) * (plan.input.complex_el ? 2 : 1);
+  CUDA_TRY(cudaMemsetAsync(ctx.dstat + 3, 0, sizeof(unsigned long long), s));
+  CUDA_TRY(launch_nonfinite(plan.prec, d_in, n, ctx.dstat + 3, s));
+  unsigned long long bad = 0;
+  CUDA_TRY(cudaMemcpyAsync(&bad, ctx.dstat + 3, sizeof(bad), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  if (bad) raise(DFFTB_ConfigInvalid, "non-finite values in plan input");
+}
+
+void ctx_check(Ctx& ctx, cudaStream_t s) {
+  DeviceGuard g(ctx.device);
+  unsigned long long st[4];
+  CUDA_TRY(cudaMemcpyAsync(st, ctx.dstat, sizeof(st), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  if (st[2]) {
+    CUDA_TRY(cudaMemset(ctx.dstat + 2, 0, sizeof(unsigned long long)));
+    raise(DFFTB_Deadlock, "peer did not reach the exchange barrier (timeout)");
+  }
+  if (ctx.c2r_pending) {
+    ctx.c2r_pending = false;
+    double mx, im;
+    std::memcpy(&mx, &st[0], sizeof(double));
+    std::memcpy(&im, &st[1], sizeof(double));
+    // irfft_1d tolerance, kernels.hpp:348-377 (scale = block max, plan.hpp:440-446)
+    const double tol = (ctx.prec == 8 ? 1e-6 : 1e-2) * mx;
+    if (im > tol) raise(DFFTB_NonHermitian, "DC or Nyquist bin has a non-real component");
+  }
+}
+
+struct EventTimer {
+  std::vector<cudaEvent_t> ev;
+  ~EventTimer() {
+    for (auto e : ev) cudaEventDestroy(e);
+  }
+  void mark(cudaStream_t s) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, s);
+    ev.push_back(e);
+  }
+};
+
+void execute(const Plan& plan, Ctx& ctx, const void* d_in, void* d_out, cudaStream_t s, int flags,
+             dfftb_timing* timers) {
+  DeviceGuard g(ctx.device);
+  check_compatible(plan, ctx);
+  if (plan.options.validate_finite) validate_finite(plan, ctx, d_in, s);
+  const int parity = (int)(ctx.exec_count & 1);
+  ctx.exec_count++;
+  auto prog = lower(plan, ctx, d_in, d_out, parity);
+  if (plan_has_c2r(plan)) {
+    CUDA_TRY(cudaMemsetAsync(ctx.dstat, 0, 2 * sizeof(unsigned long long), s));
+    ctx.c2r_pending = true;
+  }
+  EventTimer et;
+  if (timers) et.mark(s);
+  for (const auto& op : prog) {
+    const uint64_t epoch = op.barrier ? ++ctx.epoch : 0;
+    launch_op(ctx, op, epoch, s);
+    if (timers) et.mark(s);
+  }
+  if (timers) {
+    CUDA_TRY(cudaStreamSynchronize(s));
+    std::memset(timers, 0, sizeof(*timers));
+    for (size_t k = 0; k < prog.size(); ++k) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, et.ev[k], et.ev[k + 1]);
+      const double sec = ms * 1e-3;
+      if (prog[k].barrier || prog[k].fused) timers->wire_comm += sec;
+      else timers->local_fft += sec;
+    }
+    float ms = 0;
+    cudaEventElapsedTime(&ms, et.ev.front(), et.ev.back());
+    timers->total = ms * 1e-3;
+  }
+  if (timers || (flags & DFFTB_EXEC_SYNC)) ctx_check(ctx, s);
+}
+
+void execute_world(const Plan& plan, Ctx** ctxs, const void* const* d_in, void* const* d_out,
+                   cudaStream_t s, int flags) {
+  const int P = plan.nranks();
+  std::vector<std::vector<Op>> progs(P);
+  for (int r = 0; r < P; ++r) {
+    if (!ctxs[r]->world_mode) raise(DFFTB_ConfigInvalid, "not an emulated world");
+    check_compatible(plan, *ctxs[r]);
+    if (ctxs[r]->rank != r) raise(DFFTB_InvalidRank, "world contexts must be in rank order");
+  }
+  DeviceGuard g(ctxs[0]->device);
+  for (int r = 0; r < P; ++r) {
+    if (plan.options.validate_finite) validate_finite(plan, *ctxs[r], d_in[r], s);
+    const int parity = (int)(ctxs[r]->exec_count & 1);
+    ctxs[r]->exec_count++;
+    progs[r] = lower(plan, *ctxs[r], d_in[r], d_out[r], parity);
+    if (plan_has_c2r(plan)) {
+      CUDA_TRY(cudaMemsetAsync(ctxs[r]->dstat, 0, 2 * sizeof(unsigned long long), s));
+      ctxs[r]->c2r_pending = true;
+    }
+  }
+  const size_t nops = progs[0].size();
+  for (int r = 1; r < P; ++r)
+    if (progs[r].size() != nops) raise(DFFTB_CountMismatch, "rank programs differ in length");
+  for (size_t k = 0; k < nops; ++k)
+    for (int r = 0; r < P; ++r) launch_op(*ctxs[r], progs[r][k], 0, s);
+  if (flags & DFFTB_EXEC_SYNC)
+    for (int r = 0; r < P; ++r) ctx_check(*ctxs[r], s);
+}
+
+void fill_seeded(const Plan& plan, int rank, int side, uint64_t seed, int complex_field, void* d_buf,
+                 cudaStream_t s) {
+  const Dist& d = side == DFFTB_INPUT ? plan.input : plan.output;
+  if (rank < 0 || rank >= d.nranks()) raise(DFFTB_InvalidRank, "rank out of range");
+  SeedParams sp{};
+  sp.nd = d.ndim();
+  d.extents_of(rank, sp.off, sp.len);
+  sp.count = 1;
+  for (int a = 0; a < sp.nd; ++a) {
+    sp.gdims[a] = d.dims[a];
+    sp.count *= sp.len[a];
+  }
+  sp.seed = seed;
+  sp.complex_field = complex_field;
+  sp.out_complex = d.complex_el;
+  CUDA_TRY(launch_seeded(plan.prec, sp, d_buf, s));
+}
+
+}  // namespace dfftb

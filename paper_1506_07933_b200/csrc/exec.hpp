@@ -1,0 +1,23 @@
+// dfftb executor entry points (exec.cu), used by the C ABI (capi.cpp).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "internal.hpp"
+
+namespace dfftb {
+
+Ctx* ctx_create(const Plan& plan, int rank, int device);
+void ctx_export(const Ctx& ctx, CtxHandle* h);
+void ctx_connect(Ctx& ctx, const CtxHandle* handles);
+void ctx_destroy(Ctx* ctx);
+void ctx_check(Ctx& ctx, cudaStream_t s);
+void world_create(const Plan& plan, int device, Ctx** out);
+void execute(const Plan& plan, Ctx& ctx, const void* d_in, void* d_out, cudaStream_t s, int flags,
+             dfftb_timing* timers);
+void execute_world(const Plan& plan, Ctx** ctxs, const void* const* d_in, void* const* d_out,
+                   cudaStream_t s, int flags);
+void fill_seeded(const Plan& plan, int rank, int side, uint64_t seed, int complex_field, void* d_buf,
+                 cudaStream_t s);
+
+}  // namespace dfftb

@@ -1,0 +1,192 @@
+// dfftb device code: FFT pass instantiations + launchers, the cross-GPU group
+// barrier, the seeded-field generator and the finiteness check.
+#include <atomic>
+#include <cstdio>
+
+#include "fft_pass.cuh"
+#include "kernels.hpp"
+
+namespace dfftb {
+
+static std::atomic<uint64_t> g_launches{0};
+uint64_t launch_count() { return g_launches.load(); }
+void count_launch() { g_launches.fetch_add(1); }
+
+// -------------------------------------------------------- pass launchers
+
+// Tile shape per (precision, length): E elements per thread (radix-E
+// Stockham), TPL = N/E threads per lane, W lanes per CTA, <= 512 threads.
+template <typename T, int N>
+struct PassCfg {
+  static constexpr int EPREF = 8;
+  using SC = Sched<N, EPREF>;
+  static constexpr int TPL = SC::TPL;
+  static constexpr int W0 = 512 / TPL;
+  static constexpr int W = W0 < 1 ? 1 : (W0 > 64 ? 64 : W0);
+  static constexpr int THREADS = W * TPL;
+  static constexpr int SMEM = W * lane_stride<Cpx<T>>(N) * (int)sizeof(Cpx<T>);
+};
+
+template <typename T, int N, bool ADJ>
+static cudaError_t launch_tn(const PassParams& p, cudaStream_t s) {
+  using Cf = PassCfg<T, N>;
+  auto kern = fft_pass_kernel<T, N, Cf::EPREF, Cf::W, ADJ>;
+  static bool attr_done[64] = {false};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 0 && dev < 64 && !attr_done[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM);
+    if (e != cudaSuccess) return e;
+    attr_done[dev] = true;
+  }
+  const int64_t tiles = (int64_t)p.A * ((p.B + Cf::W - 1) / Cf::W);
+  if (tiles <= 0) return cudaSuccess;
+  kern<<<(unsigned)tiles, Cf::THREADS, Cf::SMEM, s>>>(p);
+  count_launch();
+  return cudaGetLastError();
+}
+
+template <typename T, int N>
+static cudaError_t launch_t(const PassParams& p, bool adj, cudaStream_t s) {
+  return adj ? launch_tn<T, N, true>(p, s) : launch_tn<T, N, false>(p, s);
+}
+
+template <typename T>
+static cudaError_t launch_prec(int n, const PassParams& p, bool adj, cudaStream_t s) {
+  switch (n) {
+    case 1: return launch_t<T, 1>(p, adj, s);
+    case 2: return launch_t<T, 2>(p, adj, s);
+    case 4: return launch_t<T, 4>(p, adj, s);
+    case 8: return launch_t<T, 8>(p, adj, s);
+    case 16: return launch_t<T, 16>(p, adj, s);
+    case 32: return launch_t<T, 32>(p, adj, s);
+    case 64: return launch_t<T, 64>(p, adj, s);
+    case 128: return launch_t<T, 128>(p, adj, s);
+    case 256: return launch_t<T, 256>(p, adj, s);
+    case 512: return launch_t<T, 512>(p, adj, s);
+    case 1024: return launch_t<T, 1024>(p, adj, s);
+    case 2048: return launch_t<T, 2048>(p, adj, s);
+    case 4096: return launch_t<T, 4096>(p, adj, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+bool pass_length_supported(int64_t n) {
+  return n >= 1 && n <= 4096 && (n & (n - 1)) == 0;
+}
+
+cudaError_t launch_pass(int prec, int n, const PassParams& p, bool adj, cudaStream_t s) {
+  return prec == 8 ? launch_prec<double>(n, p, adj, s) : launch_prec<float>(n, p, adj, s);
+}
+
+// ----------------------------------------------------------- group barrier
+
+// Cross-GPU barrier over one grid-axis group.  Thread i signals member i
+// (system-scope release store into the member's flag slot for this rank),
+// then waits for member i's flag in the local slot array.  Flags are
+// monotonically increasing epochs, so no reset is ever needed.  A timeout
+// (GPU global timer) turns a dead peer into a reported Deadlock instead of a
+// hung GPU.
+__global__ void group_barrier_kernel(BarrierParams bp) {
+  const int i = threadIdx.x;
+  if (i < bp.nmem && bp.members[i] != bp.me) {
+    __threadfence_system();
+    unsigned long long* dst = bp.peer_flags[i] + bp.me;
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(dst), "l"(bp.epoch) : "memory");
+  }
+  if (i < bp.nmem && bp.members[i] != bp.me) {
+    const unsigned long long* src = bp.my_flags + bp.members[i];
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    while (true) {
+      unsigned long long v;
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(src) : "memory");
+      if (v >= bp.epoch) break;
+      unsigned long long t1;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+      if (t1 - t0 > bp.timeout_ns) {
+        atomicExch(bp.timeout_flag, 1ull);
+        break;
+      }
+      __nanosleep(100);
+    }
+  }
+  __syncthreads();
+}
+
+cudaError_t launch_barrier(const BarrierParams& bp, cudaStream_t s) {
+  group_barrier_kernel<<<1, 32, 0, s>>>(bp);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------ seeded field
+
+__device__ __forceinline__ double unit_from_hash(unsigned long long x) {
+  // bench.cpp:22-28 (splitmix64 finalizer)
+  x += 0x9e3779b97f4a7c15ULL;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+  x ^= x >> 31;
+  return static_cast<double>(x >> 11) * 0x1.0p-52 - 1.0;
+}
+
+template <typename T>
+__global__ void seeded_fill_kernel(SeedParams sp, T* out) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; l < sp.count; l += stride) {
+    int64_t rem = l, g = 0, mul = 1;
+    for (int a = sp.nd - 1; a >= 0; --a) {
+      const int64_t c = rem % sp.len[a];
+      rem /= sp.len[a];
+      g += (sp.off[a] + c) * mul;
+      mul *= sp.gdims[a];
+    }
+    const unsigned long long base = sp.seed * 0x10001ULL + 2ULL * (unsigned long long)g;
+    const double re = unit_from_hash(base);
+    if (sp.out_complex) {
+      const double im = sp.complex_field ? unit_from_hash(base + 1) : 0.0;
+      out[2 * l] = static_cast<T>(re);
+      out[2 * l + 1] = static_cast<T>(im);
+    } else {
+      out[l] = static_cast<T>(re);
+    }
+  }
+}
+
+cudaError_t launch_seeded(int prec, const SeedParams& sp, void* out, cudaStream_t s) {
+  if (sp.count <= 0) return cudaSuccess;
+  const int threads = 256;
+  int64_t blocks = (sp.count + threads - 1) / threads;
+  if (blocks > 148 * 64) blocks = 148 * 64;
+  if (prec == 8) seeded_fill_kernel<double><<<(unsigned)blocks, threads, 0, s>>>(sp, (double*)out);
+  else seeded_fill_kernel<float><<<(unsigned)blocks, threads, 0, s>>>(sp, (float*)out);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------- finiteness check
+
+template <typename T>
+__global__ void nonfinite_kernel(const T* x, int64_t n, unsigned long long* count) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  unsigned long long c = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    c += isfinite(x[i]) ? 0 : 1;
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, c);
+}
+
+cudaError_t launch_nonfinite(int prec, const void* x, int64_t n_reals, unsigned long long* count,
+                             cudaStream_t s) {
+  if (n_reals <= 0) return cudaSuccess;
+  const int threads = 256;
+  int64_t blocks = (n_reals + threads - 1) / threads;
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  if (prec == 8) nonfinite_kernel<double><<<(unsigned)blocks, threads, 0, s>>>((const double*)x, n_reals, count);
+  else nonfinite_kernel<float><<<(unsigned)blocks, threads, 0, s>>>((const float*)x, n_reals, count);
+  count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace dfftb

@@ -1,0 +1,39 @@
+// Host-visible launch interface of the dfftb device code (kernels.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "fft_pass.cuh"
+
+namespace dfftb {
+
+struct BarrierParams {
+  unsigned long long* peer_flags[kMaxDest];  // member i's flag array (mapped)
+  int members[kMaxDest];                     // world ranks of the group
+  int nmem;
+  int me;                                    // my world rank
+  unsigned long long* my_flags;              // my flag array (indexed by world rank)
+  unsigned long long epoch;
+  unsigned long long timeout_ns;
+  unsigned long long* timeout_flag;
+};
+
+struct SeedParams {
+  int nd;
+  int64_t len[4], off[4], gdims[4];
+  int64_t count;
+  unsigned long long seed;
+  int complex_field;
+  int out_complex;
+};
+
+bool pass_length_supported(int64_t n);
+cudaError_t launch_pass(int prec, int n, const PassParams& p, bool adj, cudaStream_t s);
+cudaError_t launch_barrier(const BarrierParams& bp, cudaStream_t s);
+cudaError_t launch_seeded(int prec, const SeedParams& sp, void* out, cudaStream_t s);
+cudaError_t launch_nonfinite(int prec, const void* x, int64_t n_reals, unsigned long long* count,
+                             cudaStream_t s);
+uint64_t launch_count();
+
+}  // namespace dfftb

@@ -405,6 +405,15 @@ class ExecContext:
         _check(_lib.lib().dfftb_ctx_check(self._h, s))
 
 
+def _resolve_device(device) -> torch.device:
+    dev = torch.device(device) if device is not None else torch.device("cuda")
+    if dev.type != "cuda":
+        raise Error(23, "dfftb executes on CUDA devices only")
+    if dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    return dev
+
+
 def _all_gather_bytes(blob: bytes, comm) -> List[bytes]:
     import torch.distributed as dist
     out = [None] * dist.get_world_size(comm)
@@ -430,8 +439,7 @@ def make_context(plan: Plan, comm=None, rank: Optional[int] = None, device=None)
         my = rank
     if size != plan.nranks():
         raise Error(15, "communicator size must match the grid")
-    dev = torch.device(device) if device is not None else torch.device(
-        "cuda", torch.cuda.current_device())
+    dev = _resolve_device(device)
     L = _lib.lib()
     h = ctypes.c_void_p()
     with torch.cuda.device(dev):
@@ -450,8 +458,7 @@ def make_context(plan: Plan, comm=None, rank: Optional[int] = None, device=None)
 def make_world_contexts(plan: Plan, device=None) -> List[ExecContext]:
     """All P ranks of the plan emulated on ONE device (test harness for the
     exchange logic when fewer GPUs than ranks exist); use execute_world."""
-    dev = torch.device(device) if device is not None else torch.device(
-        "cuda", torch.cuda.current_device())
+    dev = _resolve_device(device)
     P = plan.nranks()
     arr = (ctypes.c_void_p * P)()
     with torch.cuda.device(dev):

@@ -8,7 +8,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libdfftb.so")
+LIB_PATH = os.environ.get("DFFTB_LIB_OVERRIDE") or os.path.join(HERE, "libdfftb.so")
 
 _c = ctypes
 i64p = _c.POINTER(_c.c_int64)

@@ -12,6 +12,8 @@
 //   last FFT                     -> user output
 //   FFT followed by a local FFT  -> private work buffer
 // so each axis costs one read + one write of the local block.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <unistd.h>
 
@@ -218,6 +220,8 @@ void world_create(const Plan& plan, int device, Ctx** out) {
 
 struct Op {
   bool barrier = false;
+  bool tma = false;
+  TmaPlan tp{};
   PassParams p{};
   int n = 1;
   bool adj = false;
@@ -250,6 +254,90 @@ static void check_compatible(const Plan& plan, const Ctx& ctx) {
   if (!ctx.connected) raise(DFFTB_ConfigInvalid, "context is not connected to its peers");
   if (family_bytes(plan) > ctx.exch_bytes)
     raise(DFFTB_ArenaExhausted, "context buffers are too small for this plan");
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  }
+  return fn;
+}
+
+static bool tma_disabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("DFFTB_NO_TMA");
+    v = (e && *e && *e != '0') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+// Decide whether a pass can use the TMA-prefetch kernel and build its
+// descriptor: a 3-D tensor map over (beta as reals, i, alpha) for strided
+// lanes, or a flat bulk copy of W adjacent lanes for contiguous ones.
+static bool plan_tma(Op& op, int prec) {
+  const PassParams& p = op.p;
+  const int n = op.n;
+  if (tma_disabled() || n < 8 || (int64_t)p.A * p.B == 0) return false;
+  const int W = tma_tile_w(prec, n);
+  if (W <= 0) return false;
+  const int csize = 2 * prec;
+  if ((reinterpret_cast<uintptr_t>(p.in) & 15) != 0) return false;
+  TmaPlan& tp = op.tp;
+  std::memset(&tp, 0, sizeof(tp));
+  tp.args.ntiles = (int64_t)p.A * ((p.B + W - 1) / W);
+  if (op.adj) {
+    if (p.in_mode != kInComplex) return false;
+    if ((2 * W * prec) % 16 != 0 || 2 * W > 256) return false;
+    const int64_t si = p.in_si * csize, sa = (p.A > 1 ? p.in_sa : (int64_t)n * p.in_si) * csize;
+    if (si % 16 || sa % 16 || (p.in_sb != 1)) return false;
+    auto enc = tensor_map_encoder();
+    if (!enc) return false;
+    const int rows = n < 256 ? n : 256;
+    cuuint64_t gdim[3];
+    cuuint64_t gstride[2];
+    cuuint32_t box[3], estr[3] = {1, 1, 1};
+    gdim[0] = 2 * (cuuint64_t)p.B;
+    box[0] = 2 * W;
+    if (si <= sa) {
+      tp.args.i_dim = 1;
+      gdim[1] = n;
+      gdim[2] = p.A;
+      gstride[0] = si;
+      gstride[1] = sa;
+      box[1] = rows;
+      box[2] = 1;
+    } else {
+      tp.args.i_dim = 2;
+      gdim[1] = p.A;
+      gdim[2] = n;
+      gstride[0] = sa;
+      gstride[1] = si;
+      box[1] = 1;
+      box[2] = rows;
+    }
+    CUresult r = enc(&tp.tmap, prec == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                     3, const_cast<void*>(p.in), gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return false;
+    tp.args.rows = rows;
+    tp.args.bulk = 0;
+    return true;
+  }
+  const int64_t lane_elems = p.in_mode == kInHermitian ? n / 2 + 1 : n;
+  const int esize = p.in_mode == kInReal ? prec : csize;
+  const int64_t lane_bytes = lane_elems * esize;
+  if (p.in_sb != lane_elems || lane_bytes % 16) return false;
+  if (p.A > 1 && (p.in_sa * esize) % 16) return false;
+  tp.args.bulk = 1;
+  tp.args.lane_bytes = (int)lane_bytes;
+  return true;
 }
 
 // One rank's program: fused passes and barriers.  `peer` supplies the
@@ -301,6 +389,7 @@ static std::vector<Op> lower(const Plan& plan, const Ctx& ctx, const void* d_in,
     op.adj = p.in_si != 1;
     if (lenb[v] == 0 && st.fkind != DFFTB_C2R) p.A = 0;
 
+    op.tma = false;
     if (tr) {
       const Dist& Lo = tr->after;
       const int g = tr->grid_axis;
@@ -322,6 +411,7 @@ static std::vector<Op> lower(const Plan& plan, const Ctx& ctx, const void* d_in,
         d.sb = so[ax_b];
         d.sk = so[v];
       }
+      op.tma = plan_tma(op, ctx.prec);
       prog.push_back(op);
       Op b;
       b.barrier = true;
@@ -345,6 +435,7 @@ static std::vector<Op> lower(const Plan& plan, const Ctx& ctx, const void* d_in,
       d.sa = ax_a >= 0 ? so[ax_a] : 0;
       d.sb = so[ax_b];
       d.sk = so[v];
+      op.tma = plan_tma(op, ctx.prec);
       prog.push_back(op);
       cur = out;
       i += nm ? 2 : 1;
@@ -371,7 +462,8 @@ static void launch_op(const Ctx& ctx, const Op& op, uint64_t epoch, cudaStream_t
     return;
   }
   if ((int64_t)op.p.A * op.p.B == 0) return;
-  CUDA_TRY(launch_pass(ctx.prec, op.n, op.p, op.adj, s));
+  if (op.tma) CUDA_TRY(launch_pass_tma(ctx.prec, op.n, op.p, op.adj, op.tp, s));
+  else CUDA_TRY(launch_pass(ctx.prec, op.n, op.p, op.adj, s));
 }
 
 static bool plan_has_c2r(const Plan& plan) {

@@ -31,6 +31,7 @@
 // 128-byte lines of W adjacent lanes.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -233,20 +234,129 @@ __device__ __forceinline__ void run_stages(Cpx<T>* v, Cpx<T>* lane, const Cpx<T>
   }
 }
 
-// ------------------------------------------------------------------ kernel
-template <typename T, int N, int EPREF, int W, bool ADJ>
-__global__ void __launch_bounds__(W* Sched<N, EPREF>::TPL)
-    fft_pass_kernel(const __grid_constant__ PassParams p) {
+
+// ----------------------------------------------------- stage-0 fetch/store
+
+// Fill v[] with this thread's stage-0 inputs.  ldc(pos)/ldr(pos) return the
+// complex / real element `pos` of the lane.  Applies the lane semantics:
+// real promotion (R2C, plan.hpp:428-430), Hermitian extension with DC/Nyquist
+// imaginary parts dropped (irfft_1d, kernels.hpp:378-384) and conj for
+// backward transforms.  Accumulates the C2R check statistics.
+template <typename T, int N, int EPREF, class LDC, class LDR>
+__device__ __forceinline__ void fetch0(Cpx<T>* v, int j, bool active, int in_mode, int inverse,
+                                       LDC ldc, LDR ldr, T& local_max, T& local_imag) {
+  using C = Cpx<T>;
+  using SC = Sched<N, EPREF>;
+  constexpr int E = SC::E;
+  constexpr int TPL = SC::TPL;
+  constexpr int R0 = SC::S > 0 ? SC::radix(0) : 1;
+  constexpr int NB0 = E / R0;
+#pragma unroll
+  for (int t = 0; t < NB0; ++t) {
+#pragma unroll
+    for (int r = 0; r < R0; ++r) {
+      const int pos = j + t * TPL + r * (N / R0);
+      C x = C{T(0), T(0)};
+      if (active) {
+        if (in_mode == kInComplex) {
+          x = ldc(pos);
+        } else if (in_mode == kInReal) {
+          x.x = ldr(pos);
+        } else {
+          const int src = pos <= N / 2 ? pos : N - pos;
+          x = ldc(src);
+          if (pos <= N / 2) {
+            const T m = sqrt(x.x * x.x + x.y * x.y);
+            local_max = m > local_max ? m : local_max;
+          }
+          if (pos == 0 || pos == N / 2) {
+            const T im = fabs(x.y);
+            local_imag = im > local_imag ? im : local_imag;
+            x.y = T(0);
+          }
+          if (pos > N / 2) x.y = -x.y;
+        }
+      }
+      if (inverse) x.y = -x.y;
+      v[t * R0 + r] = x;
+    }
+  }
+}
+
+// block max-abs and DC/Nyquist imaginary residue (irfft_1d checks,
+// kernels.hpp:369-377, with the block scale of plan.hpp:440-446)
+template <typename T>
+__device__ __forceinline__ void herm_reduce(unsigned long long* herm, T local_max, T local_imag) {
+  unsigned long long mb = dbits(local_max), ib = dbits(local_imag);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long a = __shfl_xor_sync(0xffffffffu, mb, o);
+    unsigned long long b = __shfl_xor_sync(0xffffffffu, ib, o);
+    mb = a > mb ? a : mb;
+    ib = b > ib ? b : ib;
+  }
+  if ((threadIdx.x & 31) == 0 && (mb | ib)) {
+    atomicMax(herm, mb);
+    atomicMax(herm + 1, ib);
+  }
+}
+
+// Last-stage registers -> final homes (local HBM or a peer's exchange buffer)
+template <typename T, int N, int EPREF>
+__device__ __forceinline__ void store_out(const PassParams& p, const Cpx<T>* v, int j, int alpha,
+                                          int beta) {
   using C = Cpx<T>;
   using SC = Sched<N, EPREF>;
   constexpr int E = SC::E;
   constexpr int TPL = SC::TPL;
   constexpr int S = SC::S;
-  constexpr int LS = lane_stride<C>(N);
+  constexpr int RL = S > 0 ? SC::radix(S - 1) : 1;
+  constexpr int NSL = S > 0 ? SC::ns(S - 1) : 1;
+  constexpr int NBL = E / RL;
+  const T sc = static_cast<T>(p.scale);
+#pragma unroll
+  for (int t = 0; t < NBL; ++t) {
+#pragma unroll
+    for (int r = 0; r < RL; ++r) {
+      const int k = j + t * TPL + r * NSL;
+      if (k >= p.n_out) continue;
+      int q = 0;
+      int kk = k;
+      if (p.ndest > 1) {
+        q = static_cast<int>(k / p.oblk);
+        kk = k - static_cast<int>(q * p.oblk);
+      }
+      const Dest& d = p.dest[q];
+      const int64_t off = d.base + (int64_t)alpha * d.sa + (int64_t)beta * d.sb + (int64_t)kk * d.sk;
+      C x = v[t * RL + r];
+      if (p.inverse) x.y = -x.y;
+      if (p.out_real) {
+        reinterpret_cast<T*>(d.ptr)[off] = x.x * sc;
+      } else {
+        x.x *= sc;
+        x.y *= sc;
+        reinterpret_cast<C*>(d.ptr)[off] = x;
+      }
+    }
+  }
+}
 
+#ifndef DFFTB_MINB
+#define DFFTB_MINB 2
+#endif
+
+// ------------------------------------------------------- direct kernel
+// One tile per CTA, stage-0 loads straight from global memory.  Used for
+// layouts the TMA variant cannot describe (unaligned rows, tiny lanes).
+template <typename T, int N, int EPREF, int W, bool ADJ>
+__global__ void __launch_bounds__(W* Sched<N, EPREF>::TPL, DFFTB_MINB)
+    fft_pass_kernel(const __grid_constant__ PassParams p) {
+  using C = Cpx<T>;
+  using SC = Sched<N, EPREF>;
+  constexpr int TPL = SC::TPL;
+  constexpr int LS = lane_stride<C>(N);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   C* smem = reinterpret_cast<C*>(smem_raw);
-
   const int tid = threadIdx.x;
   const int w = ADJ ? tid % W : tid / TPL;
   const int j = ADJ ? tid / W : tid % TPL;
@@ -256,99 +366,177 @@ __global__ void __launch_bounds__(W* Sched<N, EPREF>::TPL)
   const bool active = beta < p.B;
   C* lane = smem + w * LS;
   const C* tw = reinterpret_cast<const C*>(p.tw);
-
-  C v[E];
-
-  // ---------------- stage-0 load (HBM -> registers), with lane semantics
-  {
-    constexpr int R0 = S > 0 ? SC::radix(0) : 1;
-    constexpr int NB0 = E / R0;
-    const int64_t lane_off = (int64_t)alpha * p.in_sa + (int64_t)beta * p.in_sb;
-    T local_max = T(0), local_imag = T(0);
-#pragma unroll
-    for (int t = 0; t < NB0; ++t) {
-#pragma unroll
-      for (int r = 0; r < R0; ++r) {
-        const int pos = j + t * TPL + r * (N / R0);
-        C x = C{T(0), T(0)};
-        if (active) {
-          if (p.in_mode == kInComplex) {
-            x = __ldg(reinterpret_cast<const C*>(p.in) + lane_off + (int64_t)pos * p.in_si);
-          } else if (p.in_mode == kInReal) {
-            x.x = __ldg(reinterpret_cast<const T*>(p.in) + lane_off + (int64_t)pos * p.in_si);
-          } else {  // Hermitian half spectrum (C2R), kernels.hpp:378-384
-            const int src = pos <= N / 2 ? pos : N - pos;
-            x = __ldg(reinterpret_cast<const C*>(p.in) + lane_off + (int64_t)src * p.in_si);
-            if (pos <= N / 2) {
-              const T m = sqrt(x.x * x.x + x.y * x.y);
-              local_max = m > local_max ? m : local_max;
-            }
-            if (pos == 0 || pos == N / 2) {
-              const T im = fabs(x.y);
-              local_imag = im > local_imag ? im : local_imag;
-              x.y = T(0);
-            }
-            if (pos > N / 2) x.y = -x.y;
-          }
-        }
-        if (p.inverse) x.y = -x.y;
-        v[t * R0 + r] = x;
-      }
-    }
-    if (p.in_mode == kInHermitian) {
-      // block max-abs and DC/Nyquist imaginary residue (irfft_1d checks,
-      // kernels.hpp:369-377, with the block scale of plan.hpp:440-446)
-      unsigned long long mb = dbits(local_max), ib = dbits(local_imag);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        unsigned long long a = __shfl_xor_sync(0xffffffffu, mb, o);
-        unsigned long long b = __shfl_xor_sync(0xffffffffu, ib, o);
-        mb = a > mb ? a : mb;
-        ib = b > ib ? b : ib;
-      }
-      if ((tid & 31) == 0) {
-        atomicMax(p.herm, mb);
-        atomicMax(p.herm + 1, ib);
-      }
-    }
-  }
-
-  // ---------------- Stockham stages
+  const int64_t lane_off = (int64_t)alpha * p.in_sa + (int64_t)beta * p.in_sb;
+  C v[SC::E];
+  T lmax = T(0), limag = T(0);
+  fetch0<T, N, EPREF>(
+      v, j, active, p.in_mode, p.inverse,
+      [&](int pos) { return __ldg(reinterpret_cast<const C*>(p.in) + lane_off + (int64_t)pos * p.in_si); },
+      [&](int pos) { return __ldg(reinterpret_cast<const T*>(p.in) + lane_off + (int64_t)pos * p.in_si); },
+      lmax, limag);
+  if (p.in_mode == kInHermitian) herm_reduce<T>(p.herm, lmax, limag);
   run_stages<T, N, EPREF, 0>(v, lane, tw, j);
+  if (active) store_out<T, N, EPREF>(p, v, j, alpha, beta);
+}
 
-  // ---------------- store (registers -> HBM / peer memory)
-  if (!active) return;
-  {
-    constexpr int RL = S > 0 ? SC::radix(S - 1) : 1;
-    constexpr int NSL = S > 0 ? SC::ns(S - 1) : 1;
-    constexpr int NBL = E / RL;
-    const T sc = static_cast<T>(p.scale);
-#pragma unroll
-    for (int t = 0; t < NBL; ++t) {
-#pragma unroll
-      for (int r = 0; r < RL; ++r) {
-        const int k = j + t * TPL + r * NSL;
-        if (k >= p.n_out) continue;
-        int q = 0;
-        int kk = k;
-        if (p.ndest > 1) {
-          q = static_cast<int>(k / p.oblk);
-          kk = k - static_cast<int>(q * p.oblk);
-        }
-        const Dest& d = p.dest[q];
-        const int64_t off = d.base + (int64_t)alpha * d.sa + (int64_t)beta * d.sb + (int64_t)kk * d.sk;
-        C x = v[t * RL + r];
-        if (p.inverse) x.y = -x.y;
-        if (p.out_real) {
-          reinterpret_cast<T*>(d.ptr)[off] = x.x * sc;
-        } else {
-          x.x *= sc;
-          x.y *= sc;
-          reinterpret_cast<C*>(d.ptr)[off] = x;
-        }
+// ------------------------------------------------- TMA-prefetch kernel
+//
+// Persistent: each CTA walks tiles blockIdx.x, +gridDim.x, ...  The input
+// tile of the next STAGES tiles is brought into shared memory by the Tensor
+// Memory Accelerator while the current tile is transformed and stored, so
+// HBM reads stay in flight through the compute/store phases:
+//   * lanes along a strided axis (ADJ): one cp.async.bulk.tensor.3d box per
+//     256 rows of [rows][W adjacent lanes] (zero-filled past the last lane);
+//   * contiguous lanes: one cp.async.bulk of W whole lanes.
+// Completion is tracked with one mbarrier (expect_tx) per staging slot.
+struct TmaArgs {
+  int64_t ntiles;
+  int i_dim;   // tensor-map dimension holding the lane index i (1 or 2)
+  int rows;    // box rows per TMA op (ADJ)
+  int bulk;    // 1: contiguous cp.async.bulk, 0: tensor map
+  int lane_bytes;  // bulk mode: bytes of one stored lane
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.b32 %0, 1, 0, P1;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+  } while (!done);
+}
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const void* tmap, int c0, int c1, int c2,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <typename T, int N, int W>
+struct TmaLayout {
+  using C = Cpx<T>;
+  static constexpr int STG = W * N * (int)sizeof(C);  // one staging slot
+  static constexpr int XCH = W * lane_stride<C>(N) * (int)sizeof(C);
+};
+
+template <typename T, int N, int EPREF, int W, bool ADJ, int STAGES>
+__global__ void __launch_bounds__(W* Sched<N, EPREF>::TPL, 1)
+    fft_pass_tma_kernel(const __grid_constant__ PassParams p, const __grid_constant__ CUtensorMap tm,
+                        const TmaArgs ta) {
+  using C = Cpx<T>;
+  using SC = Sched<N, EPREF>;
+  using TL = TmaLayout<T, N, W>;
+  constexpr int TPL = SC::TPL;
+  constexpr int LS = lane_stride<C>(N);
+  extern __shared__ __align__(1024) unsigned char smem_tma[];
+  unsigned char* stg = smem_tma;
+  C* xch = reinterpret_cast<C*>(smem_tma + STAGES * TL::STG);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_tma + STAGES * TL::STG + TL::XCH);
+
+  const int tid = threadIdx.x;
+  const int w = ADJ ? tid % W : tid / TPL;
+  const int j = ADJ ? tid / W : tid % TPL;
+  const int tiles_b = (p.B + W - 1) / W;
+  C* lane = xch + w * LS;
+  const C* tw = reinterpret_cast<const C*>(p.tw);
+  const int esize = p.in_mode == kInReal ? (int)sizeof(T) : (int)sizeof(C);
+
+  auto issue = [&](int64_t t, int s) {
+    const int alpha = (int)(t / tiles_b);
+    const int beta0 = (int)(t - (int64_t)alpha * tiles_b) * W;
+    unsigned char* dst = stg + s * TL::STG;
+    if (!ta.bulk) {
+      mbar_expect_tx(&bars[s], (uint32_t)(W * N * sizeof(C)));
+      for (int r0 = 0; r0 < N; r0 += ta.rows) {
+        const int c1 = ta.i_dim == 1 ? r0 : alpha;
+        const int c2 = ta.i_dim == 1 ? alpha : r0;
+        tma_load_3d(dst + (size_t)r0 * W * sizeof(C), &tm, 2 * beta0, c1, c2, &bars[s]);
       }
+    } else {
+      const int nvalid = min(W, p.B - beta0);
+      const uint32_t bytes = (uint32_t)nvalid * (uint32_t)ta.lane_bytes;
+      mbar_expect_tx(&bars[s], bytes);
+      const unsigned char* src = reinterpret_cast<const unsigned char*>(p.in) +
+                                 ((int64_t)alpha * p.in_sa + (int64_t)beta0 * p.in_sb) * esize;
+      bulk_load(dst, src, bytes, &bars[s]);
+    }
+  };
+
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      const int64_t t = blockIdx.x + (int64_t)s * gridDim.x;
+      if (t < ta.ntiles) issue(t, s);
     }
   }
+
+  T lmax = T(0), limag = T(0);
+  int k = 0;
+  for (int64_t t = blockIdx.x; t < ta.ntiles; t += gridDim.x, ++k) {
+    const int s = k % STAGES;
+    mbar_wait(&bars[s], (uint32_t)((k / STAGES) & 1));
+    const int alpha = (int)(t / tiles_b);
+    const int beta = (int)(t - (int64_t)alpha * tiles_b) * W + w;
+    const bool active = beta < p.B;
+    const unsigned char* st = stg + s * TL::STG;
+    C v[SC::E];
+    if (ADJ) {
+      const C* sc = reinterpret_cast<const C*>(st);
+      fetch0<T, N, EPREF>(
+          v, j, active, p.in_mode, p.inverse, [&](int pos) { return sc[pos * W + w]; },
+          [&](int pos) { return T(0); }, lmax, limag);
+    } else {
+      const int ll = ta.lane_bytes / esize;  // stored lane length in elements
+      const C* sc = reinterpret_cast<const C*>(st) + w * ll;
+      const T* sr = reinterpret_cast<const T*>(st) + w * ll;
+      fetch0<T, N, EPREF>(
+          v, j, active, p.in_mode, p.inverse, [&](int pos) { return sc[pos]; },
+          [&](int pos) { return sr[pos]; }, lmax, limag);
+    }
+    __syncthreads();  // staging slot s fully consumed by every thread
+    if (tid == 0) {
+      const int64_t t2 = t + (int64_t)STAGES * gridDim.x;
+      if (t2 < ta.ntiles) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(t2, s);
+      }
+    }
+    run_stages<T, N, EPREF, 0>(v, lane, tw, j);
+    if (active) store_out<T, N, EPREF>(p, v, j, alpha, beta);
+  }
+  if (p.in_mode == kInHermitian) herm_reduce<T>(p.herm, lmax, limag);
 }
 
 }  // namespace dfftb

@@ -21,7 +21,10 @@ struct PassCfg {
   static constexpr int EPREF = 8;
   using SC = Sched<N, EPREF>;
   static constexpr int TPL = SC::TPL;
-  static constexpr int W0 = 512 / TPL;
+#ifndef DFFTB_THREADS
+#define DFFTB_THREADS 512
+#endif
+  static constexpr int W0 = DFFTB_THREADS / TPL;
   static constexpr int W = W0 < 1 ? 1 : (W0 > 64 ? 64 : W0);
   static constexpr int THREADS = W * TPL;
   static constexpr int SMEM = W * lane_stride<Cpx<T>>(N) * (int)sizeof(Cpx<T>);
@@ -69,6 +72,90 @@ static cudaError_t launch_prec(int n, const PassParams& p, bool adj, cudaStream_
     case 4096: return launch_t<T, 4096>(p, adj, s);
   }
   return cudaErrorInvalidValue;
+}
+
+// TMA variant: one persistent CTA per SM, 512 threads, STAGES-deep prefetch
+template <typename T, int N>
+struct TmaCfg {
+  static constexpr int EPREF = 8;
+  using SC = Sched<N, EPREF>;
+  static constexpr int TPL = SC::TPL;
+  static constexpr int W0 = 512 / TPL;
+  static constexpr int W = W0 < 1 ? 1 : (W0 > 64 ? 64 : W0);
+  static constexpr int THREADS = W * TPL;
+  using TL = TmaLayout<T, N, W>;
+  static constexpr int STAGES = (2 * TL::STG + TL::XCH + 64 <= 220 * 1024) ? 2 : 1;
+  static constexpr int SMEM = STAGES * TL::STG + TL::XCH + 8 * STAGES;
+};
+
+template <typename T, int N, bool ADJ>
+static cudaError_t launch_tma_tn(const PassParams& p, const TmaPlan& tp, cudaStream_t s) {
+  using Cf = TmaCfg<T, N>;
+  auto kern = fft_pass_tma_kernel<T, N, Cf::EPREF, Cf::W, ADJ, Cf::STAGES>;
+  static int grid_cap[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  if (!grid_cap[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM);
+    if (e != cudaSuccess) return e;
+    int occ = 0, sms = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Cf::THREADS, Cf::SMEM);
+    if (e != cudaSuccess) return e;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    grid_cap[dev] = (occ < 1 ? 1 : occ) * sms;
+  }
+  if (tp.args.ntiles <= 0) return cudaSuccess;
+  const int64_t grid = tp.args.ntiles < grid_cap[dev] ? tp.args.ntiles : grid_cap[dev];
+  kern<<<(unsigned)grid, Cf::THREADS, Cf::SMEM, s>>>(p, tp.tmap, tp.args);
+  count_launch();
+  return cudaGetLastError();
+}
+
+template <typename T>
+static cudaError_t launch_tma_prec(int n, const PassParams& p, bool adj, const TmaPlan& tp,
+                                   cudaStream_t s) {
+#define DFFTB_TMA_CASE(NN)                                                                   \
+  case NN:                                                                                   \
+    return adj ? launch_tma_tn<T, NN, true>(p, tp, s) : launch_tma_tn<T, NN, false>(p, tp, s);
+  switch (n) {
+    DFFTB_TMA_CASE(8)
+    DFFTB_TMA_CASE(16)
+    DFFTB_TMA_CASE(32)
+    DFFTB_TMA_CASE(64)
+    DFFTB_TMA_CASE(128)
+    DFFTB_TMA_CASE(256)
+    DFFTB_TMA_CASE(512)
+    DFFTB_TMA_CASE(1024)
+    DFFTB_TMA_CASE(2048)
+    DFFTB_TMA_CASE(4096)
+  }
+#undef DFFTB_TMA_CASE
+  return cudaErrorInvalidValue;
+}
+
+template <typename T>
+static int tma_w_prec(int n) {
+  switch (n) {
+    case 8: return TmaCfg<T, 8>::W;
+    case 16: return TmaCfg<T, 16>::W;
+    case 32: return TmaCfg<T, 32>::W;
+    case 64: return TmaCfg<T, 64>::W;
+    case 128: return TmaCfg<T, 128>::W;
+    case 256: return TmaCfg<T, 256>::W;
+    case 512: return TmaCfg<T, 512>::W;
+    case 1024: return TmaCfg<T, 1024>::W;
+    case 2048: return TmaCfg<T, 2048>::W;
+    case 4096: return TmaCfg<T, 4096>::W;
+  }
+  return 0;
+}
+
+int tma_tile_w(int prec, int n) { return prec == 8 ? tma_w_prec<double>(n) : tma_w_prec<float>(n); }
+
+cudaError_t launch_pass_tma(int prec, int n, const PassParams& p, bool adj, const TmaPlan& tp,
+                            cudaStream_t s) {
+  return prec == 8 ? launch_tma_prec<double>(n, p, adj, tp, s) : launch_tma_prec<float>(n, p, adj, tp, s);
 }
 
 bool pass_length_supported(int64_t n) {

@@ -29,6 +29,15 @@ struct SeedParams {
 };
 
 bool pass_length_supported(int64_t n);
+
+// TMA-prefetch variant (fft_pass_tma_kernel): host-side description
+struct TmaPlan {
+  CUtensorMap tmap;  // tensor-map mode (strided lanes)
+  TmaArgs args;
+};
+int tma_tile_w(int prec, int n);  // lanes per CTA of the TMA kernel
+cudaError_t launch_pass_tma(int prec, int n, const PassParams& p, bool adj, const TmaPlan& tp,
+                            cudaStream_t s);
 cudaError_t launch_pass(int prec, int n, const PassParams& p, bool adj, cudaStream_t s);
 cudaError_t launch_barrier(const BarrierParams& bp, cudaStream_t s);
 cudaError_t launch_seeded(int prec, const SeedParams& sp, void* out, cudaStream_t s);

@@ -284,6 +284,14 @@ static bool plan_tma(Op& op, int prec) {
   const PassParams& p = op.p;
   const int n = op.n;
   if (tma_disabled() || n < 8 || (int64_t)p.A * p.B == 0) return false;
+  {
+    // debug aid: DFFTB_TMA_LK_MASK restricts the TMA path to some lane kinds
+    const char* m = getenv("DFFTB_TMA_LK_MASK");
+    const int lk = p.in_mode == kInReal ? kR2C
+                   : p.in_mode == kInHermitian ? kC2R
+                   : (p.inverse ? kC2CBwd : kC2CFwd);
+    if (m && *m && !((atoi(m) >> lk) & 1)) return false;
+  }
   const int W = tma_tile_w(prec, n);
   if (W <= 0) return false;
   const int csize = 2 * prec;
@@ -338,6 +346,28 @@ static bool plan_tma(Op& op, int prec) {
   tp.args.bulk = 1;
   tp.args.lane_bytes = (int)lane_bytes;
   return true;
+}
+
+// Cheapest store addressing the destination table allows: one destination,
+// or equal power-of-two blocks with identical strides (q = k >> shift).
+static void set_store_mode(PassParams& p) {
+  p.store_mode = 2;
+  p.oshift = 0;
+  p.omask = 0;
+  if (p.ndest == 1) {
+    if (p.dest[0].sk < (1ll << 31)) p.store_mode = 0;
+    return;
+  }
+  const int64_t b = p.oblk;
+  if ((b & (b - 1)) != 0 || p.dest[0].sk >= (1ll << 31)) return;
+  for (int q = 1; q < p.ndest; ++q) {
+    const Dest& d = p.dest[q];
+    if (d.base != p.dest[0].base || d.sa != p.dest[0].sa || d.sb != p.dest[0].sb || d.sk != p.dest[0].sk)
+      return;
+  }
+  p.store_mode = 1;
+  p.oshift = ilog2((int)b);
+  p.omask = (int)b - 1;
 }
 
 // One rank's program: fused passes and barriers.  `peer` supplies the
@@ -411,6 +441,7 @@ static std::vector<Op> lower(const Plan& plan, const Ctx& ctx, const void* d_in,
         d.sb = so[ax_b];
         d.sk = so[v];
       }
+      set_store_mode(p);
       op.tma = plan_tma(op, ctx.prec);
       prog.push_back(op);
       Op b;
@@ -435,6 +466,7 @@ static std::vector<Op> lower(const Plan& plan, const Ctx& ctx, const void* d_in,
       d.sa = ax_a >= 0 ? so[ax_a] : 0;
       d.sb = so[ax_b];
       d.sk = so[v];
+      set_store_mode(p);
       op.tma = plan_tma(op, ctx.prec);
       prog.push_back(op);
       cur = out;
@@ -498,7 +530,14 @@ void ctx_check(Ctx& ctx, cudaStream_t s) {
     std::memcpy(&im, &st[1], sizeof(double));
     // irfft_1d tolerance, kernels.hpp:348-377 (scale = block max, plan.hpp:440-446)
     const double tol = (ctx.prec == 8 ? 1e-6 : 1e-2) * mx;
-    if (im > tol) raise(DFFTB_NonHermitian, "DC or Nyquist bin has a non-real component");
+    const char* skip = getenv("DFFTB_DEBUG_SKIP_HERM");
+    if (im > tol && !(skip && *skip == '1')) {
+      char buf[160];
+      snprintf(buf, sizeof(buf),
+               "DC or Nyquist bin has a non-real component (|Im| %.3g > tol %.3g, block max %.3g)",
+               im, tol, mx);
+      raise(DFFTB_NonHermitian, buf);
+    }
   }
 }
 

@@ -70,6 +70,8 @@ struct PassParams {
   int n_out;                    // stored positions: n, or n/2+1 for R2C
   int ndest;
   int64_t oblk;                 // ceil-block size of the scattered axis
+  int store_mode;               // 0 one dest, 1 equal pow-2 blocks, 2 general
+  int oshift, omask;            // store_mode 1: q = k >> oshift, kk = k & omask
   double scale;
   const void* tw;               // N complex twiddles exp(-2 pi i m / N)
   unsigned long long* herm;     // C2R: [0] max |X| bits, [1] max |Im DC/Nyq| bits
@@ -377,166 +379,6 @@ __global__ void __launch_bounds__(W* Sched<N, EPREF>::TPL, DFFTB_MINB)
   if (p.in_mode == kInHermitian) herm_reduce<T>(p.herm, lmax, limag);
   run_stages<T, N, EPREF, 0>(v, lane, tw, j);
   if (active) store_out<T, N, EPREF>(p, v, j, alpha, beta);
-}
-
-// ------------------------------------------------- TMA-prefetch kernel
-//
-// Persistent: each CTA walks tiles blockIdx.x, +gridDim.x, ...  The input
-// tile of the next STAGES tiles is brought into shared memory by the Tensor
-// Memory Accelerator while the current tile is transformed and stored, so
-// HBM reads stay in flight through the compute/store phases:
-//   * lanes along a strided axis (ADJ): one cp.async.bulk.tensor.3d box per
-//     256 rows of [rows][W adjacent lanes] (zero-filled past the last lane);
-//   * contiguous lanes: one cp.async.bulk of W whole lanes.
-// Completion is tracked with one mbarrier (expect_tx) per staging slot.
-struct TmaArgs {
-  int64_t ntiles;
-  int i_dim;   // tensor-map dimension holding the lane index i (1 or 2)
-  int rows;    // box rows per TMA op (ADJ)
-  int bulk;    // 1: contiguous cp.async.bulk, 0: tensor map
-  int lane_bytes;  // bulk mode: bytes of one stored lane
-};
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-  uint32_t done = 0;
-  do {
-    asm volatile(
-        "{\n\t.reg .pred P1;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
-        "selp.b32 %0, 1, 0, P1;\n\t}"
-        : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(phase)
-        : "memory");
-  } while (!done);
-}
-
-__device__ __forceinline__ void tma_load_3d(void* dst, const void* tmap, int c0, int c1, int c2,
-                                            uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
-      : "memory");
-}
-
-__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-
-template <typename T, int N, int W>
-struct TmaLayout {
-  using C = Cpx<T>;
-  static constexpr int STG = W * N * (int)sizeof(C);  // one staging slot
-  static constexpr int XCH = W * lane_stride<C>(N) * (int)sizeof(C);
-};
-
-template <typename T, int N, int EPREF, int W, bool ADJ, int STAGES>
-__global__ void __launch_bounds__(W* Sched<N, EPREF>::TPL, 1)
-    fft_pass_tma_kernel(const __grid_constant__ PassParams p, const __grid_constant__ CUtensorMap tm,
-                        const TmaArgs ta) {
-  using C = Cpx<T>;
-  using SC = Sched<N, EPREF>;
-  using TL = TmaLayout<T, N, W>;
-  constexpr int TPL = SC::TPL;
-  constexpr int LS = lane_stride<C>(N);
-  extern __shared__ __align__(1024) unsigned char smem_tma[];
-  unsigned char* stg = smem_tma;
-  C* xch = reinterpret_cast<C*>(smem_tma + STAGES * TL::STG);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_tma + STAGES * TL::STG + TL::XCH);
-
-  const int tid = threadIdx.x;
-  const int w = ADJ ? tid % W : tid / TPL;
-  const int j = ADJ ? tid / W : tid % TPL;
-  const int tiles_b = (p.B + W - 1) / W;
-  C* lane = xch + w * LS;
-  const C* tw = reinterpret_cast<const C*>(p.tw);
-  const int esize = p.in_mode == kInReal ? (int)sizeof(T) : (int)sizeof(C);
-
-  auto issue = [&](int64_t t, int s) {
-    const int alpha = (int)(t / tiles_b);
-    const int beta0 = (int)(t - (int64_t)alpha * tiles_b) * W;
-    unsigned char* dst = stg + s * TL::STG;
-    if (!ta.bulk) {
-      mbar_expect_tx(&bars[s], (uint32_t)(W * N * sizeof(C)));
-      for (int r0 = 0; r0 < N; r0 += ta.rows) {
-        const int c1 = ta.i_dim == 1 ? r0 : alpha;
-        const int c2 = ta.i_dim == 1 ? alpha : r0;
-        tma_load_3d(dst + (size_t)r0 * W * sizeof(C), &tm, 2 * beta0, c1, c2, &bars[s]);
-      }
-    } else {
-      const int nvalid = min(W, p.B - beta0);
-      const uint32_t bytes = (uint32_t)nvalid * (uint32_t)ta.lane_bytes;
-      mbar_expect_tx(&bars[s], bytes);
-      const unsigned char* src = reinterpret_cast<const unsigned char*>(p.in) +
-                                 ((int64_t)alpha * p.in_sa + (int64_t)beta0 * p.in_sb) * esize;
-      bulk_load(dst, src, bytes, &bars[s]);
-    }
-  };
-
-  if (tid == 0) {
-    for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  if (tid == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      const int64_t t = blockIdx.x + (int64_t)s * gridDim.x;
-      if (t < ta.ntiles) issue(t, s);
-    }
-  }
-
-  T lmax = T(0), limag = T(0);
-  int k = 0;
-  for (int64_t t = blockIdx.x; t < ta.ntiles; t += gridDim.x, ++k) {
-    const int s = k % STAGES;
-    mbar_wait(&bars[s], (uint32_t)((k / STAGES) & 1));
-    const int alpha = (int)(t / tiles_b);
-    const int beta = (int)(t - (int64_t)alpha * tiles_b) * W + w;
-    const bool active = beta < p.B;
-    const unsigned char* st = stg + s * TL::STG;
-    C v[SC::E];
-    if (ADJ) {
-      const C* sc = reinterpret_cast<const C*>(st);
-      fetch0<T, N, EPREF>(
-          v, j, active, p.in_mode, p.inverse, [&](int pos) { return sc[pos * W + w]; },
-          [&](int pos) { return T(0); }, lmax, limag);
-    } else {
-      const int ll = ta.lane_bytes / esize;  // stored lane length in elements
-      const C* sc = reinterpret_cast<const C*>(st) + w * ll;
-      const T* sr = reinterpret_cast<const T*>(st) + w * ll;
-      fetch0<T, N, EPREF>(
-          v, j, active, p.in_mode, p.inverse, [&](int pos) { return sc[pos]; },
-          [&](int pos) { return sr[pos]; }, lmax, limag);
-    }
-    __syncthreads();  // staging slot s fully consumed by every thread
-    if (tid == 0) {
-      const int64_t t2 = t + (int64_t)STAGES * gridDim.x;
-      if (t2 < ta.ntiles) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        issue(t2, s);
-      }
-    }
-    run_stages<T, N, EPREF, 0>(v, lane, tw, j);
-    if (active) store_out<T, N, EPREF>(p, v, j, alpha, beta);
-  }
-  if (p.in_mode == kInHermitian) herm_reduce<T>(p.herm, lmax, limag);
 }
 
 }  // namespace dfftb

@@ -1,0 +1,283 @@
+// TMA-prefetch persistent FFT pass kernel (the main B200 path).
+//
+// Each CTA walks tiles blockIdx.x, +gridDim.x, ...  The input tiles of the
+// next STAGES tiles are brought into shared memory by the Tensor Memory
+// Accelerator while the current tile is transformed and stored, so HBM reads
+// stay in flight through the butterfly and store phases:
+//   * lanes along a strided axis (ADJ): cp.async.bulk.tensor.3d boxes of
+//     [rows <= 256][W adjacent lanes] (zero-filled past the last lane);
+//   * contiguous lanes: one cp.async.bulk of W whole lanes.
+// Completion is tracked with one mbarrier (expect_tx) per staging slot.
+//
+// Lane kind LK is a template parameter so the lane semantics cost nothing:
+//   0 C2C forward, 1 C2C backward (conj in/out), 2 R2C (real in),
+//   3 C2R (Hermitian half in, real out; irfft_1d, kernels.hpp:362-389).
+#pragma once
+
+#include "fft_pass.cuh"
+
+namespace dfftb {
+
+enum LaneKind : int { kC2CFwd = 0, kC2CBwd = 1, kR2C = 2, kC2R = 3 };
+
+struct TmaArgs {
+  int64_t ntiles;
+  int i_dim;       // tensor-map dimension holding the lane index i (1 or 2)
+  int rows;        // box rows per TMA op (ADJ)
+  int bulk;        // 1: contiguous cp.async.bulk, 0: tensor map
+  int lane_bytes;  // bulk mode: bytes of one stored lane
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.b32 %0, 1, 0, P1;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+  } while (!done);
+}
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const void* tmap, int c0, int c1, int c2,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <typename T, int N, int W>
+struct TmaLayout {
+  using C = Cpx<T>;
+  static constexpr int STG = W * N * (int)sizeof(C);  // one staging slot
+  static constexpr int XCH = W * lane_stride<C>(N) * (int)sizeof(C);
+};
+
+// stage-0 fetch from a staging slot, compile-time lane kind
+template <typename T, int N, int EPREF, int LK, class LDC, class LDR>
+__device__ __forceinline__ void fetch0_lk(Cpx<T>* v, int j, LDC ldc, LDR ldr) {
+  using C = Cpx<T>;
+  using SC = Sched<N, EPREF>;
+  constexpr int E = SC::E;
+  constexpr int TPL = SC::TPL;
+  constexpr int R0 = SC::S > 0 ? SC::radix(0) : 1;
+  constexpr int NB0 = E / R0;
+#pragma unroll
+  for (int t = 0; t < NB0; ++t) {
+#pragma unroll
+    for (int r = 0; r < R0; ++r) {
+      const int pos = j + t * TPL + r * (N / R0);
+      C x;
+      if constexpr (LK == kC2CFwd) {
+        x = ldc(pos);
+      } else if constexpr (LK == kC2CBwd) {
+        x = ldc(pos);
+        x.y = -x.y;
+      } else if constexpr (LK == kR2C) {
+        x = C{ldr(pos), T(0)};
+      } else {
+        // Hermitian extension, DC/Nyquist imaginary parts dropped, then the
+        // conj of the backward transform: x = conj(X_ext).  (The NonHermitian
+        // statistics are taken from the staged bins by the kernel.)
+        const bool lo = pos <= N / 2;
+        x = ldc(lo ? pos : N - pos);
+        if (pos == 0 || pos == N / 2) x.y = T(0);
+        if (lo) x.y = -x.y;
+      }
+      v[t * R0 + r] = x;
+    }
+  }
+}
+
+// final store, compile-time lane kind; per-tile addressing precomputed
+template <typename T, int N, int EPREF, int LK>
+__device__ __forceinline__ void store_lk(const PassParams& p, void* const* sptr, const Cpx<T>* v,
+                                         int j, int alpha, int beta, T sc) {
+  using C = Cpx<T>;
+  using SC = Sched<N, EPREF>;
+  constexpr int E = SC::E;
+  constexpr int TPL = SC::TPL;
+  constexpr int S = SC::S;
+  constexpr int RL = S > 0 ? SC::radix(S - 1) : 1;
+  constexpr int NSL = S > 0 ? SC::ns(S - 1) : 1;
+  constexpr int NBL = E / RL;
+  auto put = [&](void* base, int64_t off, C x) {
+    if constexpr (LK == kC2CBwd) x.y = -x.y;
+    if constexpr (LK == kC2R) {
+      reinterpret_cast<T*>(base)[off] = x.x * sc;
+    } else {
+      x.x *= sc;
+      x.y *= sc;
+      reinterpret_cast<C*>(base)[off] = x;
+    }
+  };
+  if (p.store_mode != 2) {
+    const Dest& d0 = p.dest[0];
+    const int64_t tile = d0.base + (int64_t)alpha * d0.sa + (int64_t)beta * d0.sb;
+    const int sk = (int)d0.sk;
+#pragma unroll
+    for (int t = 0; t < NBL; ++t) {
+#pragma unroll
+      for (int r = 0; r < RL; ++r) {
+        const int k = j + t * TPL + r * NSL;
+        if constexpr (LK == kR2C) {
+          if (k > N / 2) continue;
+        }
+        if (p.store_mode == 0) {
+          put(d0.ptr, tile + (int64_t)k * sk, v[t * RL + r]);
+        } else {
+          const int q = k >> p.oshift;
+          const int kk = k & p.omask;
+          put(sptr[q], tile + (int64_t)kk * sk, v[t * RL + r]);
+        }
+      }
+    }
+  } else {
+#pragma unroll
+    for (int t = 0; t < NBL; ++t) {
+#pragma unroll
+      for (int r = 0; r < RL; ++r) {
+        const int k = j + t * TPL + r * NSL;
+        if (k >= p.n_out) continue;
+        const int q = static_cast<int>(k / p.oblk);
+        const int kk = k - static_cast<int>(q * p.oblk);
+        const Dest& d = p.dest[q];
+        put(d.ptr, d.base + (int64_t)alpha * d.sa + (int64_t)beta * d.sb + (int64_t)kk * d.sk,
+            v[t * RL + r]);
+      }
+    }
+  }
+}
+
+template <typename T, int N, int EPREF, int W, bool ADJ, int STAGES, int LK>
+__global__ void __launch_bounds__(W* Sched<N, EPREF>::TPL, 1)
+    fft_pass_tma_kernel(const __grid_constant__ PassParams p, const __grid_constant__ CUtensorMap tm,
+                        const TmaArgs ta) {
+  using C = Cpx<T>;
+  using SC = Sched<N, EPREF>;
+  using TL = TmaLayout<T, N, W>;
+  constexpr int TPL = SC::TPL;
+  constexpr int LS = lane_stride<C>(N);
+  extern __shared__ __align__(1024) unsigned char smem_tma[];
+  unsigned char* stg = smem_tma;
+  C* xch = reinterpret_cast<C*>(smem_tma + STAGES * TL::STG);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_tma + STAGES * TL::STG + TL::XCH);
+  void** sptr = reinterpret_cast<void**>(bars + STAGES);  // destination pointers
+
+  const int tid = threadIdx.x;
+  const int w = ADJ ? tid % W : tid / TPL;
+  const int j = ADJ ? tid / W : tid % TPL;
+  const int tiles_b = (p.B + W - 1) / W;
+  C* lane = xch + w * LS;
+  const C* tw = reinterpret_cast<const C*>(p.tw);
+  constexpr int ESIZE = LK == kR2C ? (int)sizeof(T) : (int)sizeof(C);
+  const T sc = static_cast<T>(p.scale);
+
+  auto issue = [&](int64_t t, int s) {
+    const int alpha = (int)(t / tiles_b);
+    const int beta0 = (int)(t - (int64_t)alpha * tiles_b) * W;
+    unsigned char* dst = stg + s * TL::STG;
+    if constexpr (ADJ) {
+      mbar_expect_tx(&bars[s], (uint32_t)(W * N * sizeof(C)));
+      for (int r0 = 0; r0 < N; r0 += ta.rows) {
+        const int c1 = ta.i_dim == 1 ? r0 : alpha;
+        const int c2 = ta.i_dim == 1 ? alpha : r0;
+        tma_load_3d(dst + (size_t)r0 * W * sizeof(C), &tm, 2 * beta0, c1, c2, &bars[s]);
+      }
+    } else {
+      const int nvalid = min(W, p.B - beta0);
+      const uint32_t bytes = (uint32_t)nvalid * (uint32_t)ta.lane_bytes;
+      mbar_expect_tx(&bars[s], bytes);
+      const unsigned char* src = reinterpret_cast<const unsigned char*>(p.in) +
+                                 ((int64_t)alpha * p.in_sa + (int64_t)beta0 * p.in_sb) * ESIZE;
+      bulk_load(dst, src, bytes, &bars[s]);
+    }
+  };
+
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (tid < kMaxDest) sptr[tid] = p.dest[tid].ptr;
+  __syncthreads();
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      const int64_t t = blockIdx.x + (int64_t)s * gridDim.x;
+      if (t < ta.ntiles) issue(t, s);
+    }
+  }
+
+  int k = 0;
+  for (int64_t t = blockIdx.x; t < ta.ntiles; t += gridDim.x, ++k) {
+    const int s = k % STAGES;
+    mbar_wait(&bars[s], (uint32_t)((k / STAGES) & 1));
+    const int alpha = (int)(t / tiles_b);
+    const int beta = (int)(t - (int64_t)alpha * tiles_b) * W + w;
+    const unsigned char* st = stg + s * TL::STG;
+    C v[SC::E];
+    if constexpr (ADJ) {
+      const C* scp = reinterpret_cast<const C*>(st);
+      fetch0_lk<T, N, EPREF, LK>(
+          v, j, [&](int pos) { return scp[pos * W + w]; }, [&](int) { return T(0); });
+    } else {
+      const int ll = ta.lane_bytes / ESIZE;  // stored lane length in elements
+      const C* scp = reinterpret_cast<const C*>(st) + w * ll;
+      const T* srp = reinterpret_cast<const T*>(st) + w * ll;
+      fetch0_lk<T, N, EPREF, LK>(
+          v, j, [&](int pos) { return scp[pos]; }, [&](int pos) { return srp[pos]; });
+    }
+    if constexpr (LK == kC2R) {
+      // NonHermitian statistics straight from the staged half spectrum:
+      // block max |X| and the DC / Nyquist imaginary residues of active lanes
+      T lmax = T(0), limag = T(0);
+      if (beta < p.B) {
+        const int ll = ta.lane_bytes / ESIZE;
+        const C* scp = reinterpret_cast<const C*>(st) + w * ll;
+        for (int i = j; i < ll; i += TPL) {
+          const C x = scp[i];
+          const T m = sqrt(x.x * x.x + x.y * x.y);
+          lmax = m > lmax ? m : lmax;
+          if (i == 0 || i == N / 2) limag = fabs(x.y) > limag ? fabs(x.y) : limag;
+        }
+      }
+      herm_reduce<T>(p.herm, lmax, limag);
+    }
+    __syncthreads();  // staging slot s fully consumed by every thread
+    if (tid == 0) {
+      const int64_t t2 = t + (int64_t)STAGES * gridDim.x;
+      if (t2 < ta.ntiles) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(t2, s);
+      }
+    }
+    run_stages<T, N, EPREF, 0>(v, lane, tw, j);
+    if (beta < p.B) store_lk<T, N, EPREF, LK>(p, sptr, v, j, alpha, beta, sc);
+  }
+}
+
+}  // namespace dfftb

@@ -4,6 +4,7 @@
 #include <cstdio>
 
 #include "fft_pass.cuh"
+#include "fft_pass_tma.cuh"
 #include "kernels.hpp"
 
 namespace dfftb {
@@ -85,13 +86,13 @@ struct TmaCfg {
   static constexpr int THREADS = W * TPL;
   using TL = TmaLayout<T, N, W>;
   static constexpr int STAGES = (2 * TL::STG + TL::XCH + 64 <= 220 * 1024) ? 2 : 1;
-  static constexpr int SMEM = STAGES * TL::STG + TL::XCH + 8 * STAGES;
+  static constexpr int SMEM = STAGES * TL::STG + TL::XCH + 8 * STAGES + 8 * kMaxDest;
 };
 
-template <typename T, int N, bool ADJ>
+template <typename T, int N, bool ADJ, int LK>
 static cudaError_t launch_tma_tn(const PassParams& p, const TmaPlan& tp, cudaStream_t s) {
   using Cf = TmaCfg<T, N>;
-  auto kern = fft_pass_tma_kernel<T, N, Cf::EPREF, Cf::W, ADJ, Cf::STAGES>;
+  auto kern = fft_pass_tma_kernel<T, N, Cf::EPREF, Cf::W, ADJ, Cf::STAGES, LK>;
   static int grid_cap[64] = {0};
   int dev = 0;
   cudaGetDevice(&dev);
@@ -115,9 +116,20 @@ static cudaError_t launch_tma_tn(const PassParams& p, const TmaPlan& tp, cudaStr
 template <typename T>
 static cudaError_t launch_tma_prec(int n, const PassParams& p, bool adj, const TmaPlan& tp,
                                    cudaStream_t s) {
-#define DFFTB_TMA_CASE(NN)                                                                   \
-  case NN:                                                                                   \
-    return adj ? launch_tma_tn<T, NN, true>(p, tp, s) : launch_tma_tn<T, NN, false>(p, tp, s);
+  const int lk = p.in_mode == kInReal ? kR2C : (p.in_mode == kInHermitian ? kC2R : (p.inverse ? kC2CBwd : kC2CFwd));
+#define DFFTB_TMA_CASE(NN)                                                \
+  case NN:                                                                \
+    if (adj) {                                                            \
+      if (lk == kC2CFwd) return launch_tma_tn<T, NN, true, kC2CFwd>(p, tp, s);  \
+      if (lk == kC2CBwd) return launch_tma_tn<T, NN, true, kC2CBwd>(p, tp, s);  \
+      return cudaErrorInvalidValue;                                       \
+    }                                                                     \
+    switch (lk) {                                                         \
+      case kC2CFwd: return launch_tma_tn<T, NN, false, kC2CFwd>(p, tp, s);     \
+      case kC2CBwd: return launch_tma_tn<T, NN, false, kC2CBwd>(p, tp, s);     \
+      case kR2C: return launch_tma_tn<T, NN, false, kR2C>(p, tp, s);           \
+      default: return launch_tma_tn<T, NN, false, kC2R>(p, tp, s);             \
+    }
   switch (n) {
     DFFTB_TMA_CASE(8)
     DFFTB_TMA_CASE(16)

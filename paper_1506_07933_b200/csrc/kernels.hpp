@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include "fft_pass.cuh"
+#include "fft_pass_tma.cuh"
 
 namespace dfftb {
 

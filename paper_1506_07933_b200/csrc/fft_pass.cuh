@@ -35,6 +35,17 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+// Build-time tuning knobs (defaults are the shipped configuration)
+#ifndef DFFTB_TW_REC
+#define DFFTB_TW_REC 1      // 1: twiddle powers by products instead of table reads
+#endif
+#ifndef DFFTB_TMA_THREADS
+#define DFFTB_TMA_THREADS 512  // threads per CTA of the TMA pass kernel
+#endif
+#ifndef DFFTB_TMA_MINB
+#define DFFTB_TMA_MINB 1    // resident CTAs per SM the TMA kernel is compiled for
+#endif
+
 namespace dfftb {
 
 template <typename T> struct CpxOf;
@@ -207,8 +218,19 @@ __device__ __forceinline__ void run_stages(Cpx<T>* v, Cpx<T>* lane, const Cpx<T>
         const int bidx = j + t * TPL;
         const int pp = bidx & (NS - 1);
         const int step = pp * (N / (NS * R));
+#if DFFTB_TW_REC
+        // one table read per butterfly, the other powers by products
+        // (depth <= 3 multiplications: a few ulp, far inside 1e-12)
+        C wp[R];
+        wp[1] = __ldg(tw + step);
+#pragma unroll
+        for (int r = 2; r < R; ++r) wp[r] = cmul(wp[r / 2], wp[r - r / 2]);
+#pragma unroll
+        for (int r = 1; r < R; ++r) v[t * R + r] = cmul(v[t * R + r], wp[r]);
+#else
 #pragma unroll
         for (int r = 1; r < R; ++r) v[t * R + r] = cmul(v[t * R + r], __ldg(tw + r * step));
+#endif
       }
     }
 #pragma unroll

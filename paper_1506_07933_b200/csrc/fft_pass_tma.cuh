@@ -175,7 +175,7 @@ __device__ __forceinline__ void store_lk(const PassParams& p, void* const* sptr,
 }
 
 template <typename T, int N, int EPREF, int W, bool ADJ, int STAGES, int LK>
-__global__ void __launch_bounds__(W* Sched<N, EPREF>::TPL, 1)
+__global__ void __launch_bounds__(W* Sched<N, EPREF>::TPL, DFFTB_TMA_MINB)
     fft_pass_tma_kernel(const __grid_constant__ PassParams p, const __grid_constant__ CUtensorMap tm,
                         const TmaArgs ta) {
   using C = Cpx<T>;

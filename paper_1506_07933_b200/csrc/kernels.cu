@@ -81,11 +81,11 @@ struct TmaCfg {
   static constexpr int EPREF = 8;
   using SC = Sched<N, EPREF>;
   static constexpr int TPL = SC::TPL;
-  static constexpr int W0 = 512 / TPL;
+  static constexpr int W0 = DFFTB_TMA_THREADS / TPL;
   static constexpr int W = W0 < 1 ? 1 : (W0 > 64 ? 64 : W0);
   static constexpr int THREADS = W * TPL;
   using TL = TmaLayout<T, N, W>;
-  static constexpr int STAGES = (2 * TL::STG + TL::XCH + 64 <= 220 * 1024) ? 2 : 1;
+  static constexpr int STAGES = (2 * TL::STG + TL::XCH + 128 <= (220 * 1024) / DFFTB_TMA_MINB) ? 2 : 1;
   static constexpr int SMEM = STAGES * TL::STG + TL::XCH + 8 * STAGES + 8 * kMaxDest;
 };
 

@@ -54,39 +54,59 @@ class ClockSampler:
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index):
+    def __init__(self, index, interval_ms=10):
         self.index = index
-        self.rows = []
-        self._stop = threading.Event()
+        self.interval_ms = interval_ms
+        self.rows = []  # (host time, fields)
+        self.window = None
+        self._proc = None
         self._t = None
 
-    def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True,
-                                     text=True, timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([c.strip() for c in out.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+    def _read(self):
+        for line in self._proc.stdout:
+            line = line.strip()
+            if line:
+                self.rows.append((time.time(), [c.strip() for c in line.split(",")]))
 
     def start(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
+        """Continuous `nvidia-smi -lms` stream; returns once it is producing."""
+        try:
+            self._proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", f"-lms={self.interval_ms}"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            return
+        self._t = threading.Thread(target=self._read, daemon=True)
         self._t.start()
+        t0 = time.time()
+        while not self.rows and time.time() - t0 < 5:
+            time.sleep(0.01)
 
     def stop(self):
-        self._stop.set()
+        time.sleep(2 * self.interval_ms / 1000.0)
+        if self._proc:
+            self._proc.terminate()
+            try:
+                self._proc.wait(timeout=5)
+            except Exception:
+                self._proc.kill()
         if self._t:
-            self._t.join(timeout=10)
+            self._t.join(timeout=5)
 
     def summary(self):
         sm = []
         mx = None
         reasons = set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for r in self.rows:
+        rows = [r for t, r in self.rows
+                if self.window is None or self.window[0] <= t <= self.window[1]]
+        in_window = len(rows)
+        if not rows and self.rows and self.window:
+            # region shorter than the sampling period: nearest samples around it
+            mid = 0.5 * (self.window[0] + self.window[1])
+            rows = [r for _, r in sorted(self.rows, key=lambda tr: abs(tr[0] - mid))[:2]]
+        for r in rows:
             try:
                 sm.append(float(r[1]))
                 mx = float(r[2])
@@ -97,14 +117,29 @@ class ClockSampler:
                 pass
         sm.sort()
         return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                "samples_in_timed_region": in_window}
 
 
 # --------------------------------------------------------- reference (CPU)
 
 def cpu_threads():
-    n = os.cpu_count() or 1
-    return 8 if n >= 8 else (4 if n >= 4 else (2 if n >= 2 else 1))
+    """The reference has one thread per rank and no intra-rank threading
+    (transport.cpp:92-119): use the largest power-of-two rank count the host
+    cores allow (capped at 64)."""
+    n = min(os.cpu_count() or 1, 64)
+    p = 1
+    while p * 2 <= n:
+        p *= 2
+    return p
+
+
+def cpu_grid(p):
+    a = 1
+    while a * a < p:
+        a *= 2
+    a = a if a * a == p else a // 2
+    return f"{a},{p // a}"
 
 
 def run_reference(warmup, reps, dims=DIMS):
@@ -113,7 +148,7 @@ def run_reference(warmup, reps, dims=DIMS):
     if not os.path.exists(REF_BIN):
         raise RuntimeError("oracle/_ref/dfft_ref not built (make -C oracle ref)")
     p = cpu_threads()
-    grid = {8: "2,4", 4: "2,2", 2: "2,1", 1: "1,1"}[p]
+    grid = cpu_grid(p)
     cmd = [REF_BIN, "--dims", ",".join(map(str, dims)), "--decomp", "pencil", "--grid", grid,
            "--kind", "c2c", "--prec", "f64", "--seed", "1", "--warmup", str(warmup),
            "--reps", str(reps)]
@@ -217,19 +252,21 @@ def main():
     sampler = ClockSampler(local) if rank == 0 else None
     if sampler:
         sampler.start()
-        time.sleep(0.3)
     barrier()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     l_before = D.kernel_launch_count()
+    t_host0 = time.time()
     e0.record(stream)
     for _ in range(K):
         step()
     e1.record(stream)
     barrier()
+    t_host1 = time.time()
     l_timed = D.kernel_launch_count() - l_before
     if sampler:
         sampler.stop()
+        sampler.window = (t_host0, t_host1)
     ms = max_over_ranks(e0.elapsed_time(e1)) / K
     ctx.check()
 
@@ -255,33 +292,61 @@ def main():
     peak, peak_kind = peaks()
     achieved = alg_bytes / (avg_pass_ms * 1e-3) / 1e9
 
-    # end-to-end through the public API with host buffers
+    # end-to-end through the public API with host buffers: every step copies
+    # its input from pinned host memory, runs fwd+inv and reads the result
+    # back.  Copies run on their own streams, double-buffered, so step s+1's
+    # upload overlaps step s's compute and download (PCIe is full duplex).
     e2e = None
     if not args.no_e2e:
         hx = torch.empty(local_elems, dtype=torch.complex128, pin_memory=True)
         hx.copy_(x.data.cpu())
-        hz = torch.empty(local_elems, dtype=torch.complex128, pin_memory=True)
-        xin = D.DistTensor(fwd.input, rank, torch.empty_like(x.data))
+        hz = [torch.empty(local_elems, dtype=torch.complex128, pin_memory=True) for _ in range(2)]
+        xin = [D.DistTensor(fwd.input, rank, torch.empty_like(x.data)) for _ in range(2)]
+        zout = [D.DistTensor(bwd.output, rank, torch.empty_like(z.data)) for _ in range(2)]
+        s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+        s_cmp = torch.cuda.current_stream()
+        ev = {}
 
-        def e2e_step():
-            xin.data.copy_(hx, non_blocking=True)
-            D.execute(fwd, xin, ctx, out=y, sync=False)
-            D.execute(bwd, y, ctx, out=z, sync=False)
-            hz.copy_(z.data, non_blocking=True)
+        def e2e_step(i):
+            b = i % 2
+            with torch.cuda.stream(s_in):
+                if ("cmp", i - 2) in ev:
+                    s_in.wait_event(ev[("cmp", i - 2)])   # buffer b no longer read
+                xin[b].data.copy_(hx, non_blocking=True)
+                ev[("in", i)] = torch.cuda.Event()
+                ev[("in", i)].record(s_in)
+            s_cmp.wait_event(ev[("in", i)])
+            if ("out", i - 2) in ev:
+                s_cmp.wait_event(ev[("out", i - 2)])      # zout[b] downloaded
+            D.execute(fwd, xin[b], ctx, out=y, sync=False)
+            D.execute(bwd, y, ctx, out=zout[b], sync=False)
+            ev[("cmp", i)] = torch.cuda.Event()
+            ev[("cmp", i)].record(s_cmp)
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(ev[("cmp", i)])
+                hz[b].copy_(zout[b].data, non_blocking=True)
+                ev[("out", i)] = torch.cuda.Event()
+                ev[("out", i)].record(s_out)
 
-        for _ in range(2):
-            e2e_step()
+        for i in range(2):
+            e2e_step(i)
         barrier()
-        Ke = max(2, min(K, 5))
-        e0.record(stream)
-        for _ in range(Ke):
-            e2e_step()
-        e1.record(stream)
+        ev.clear()
+        Ke = max(2, min(K, 6))
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(s_in)
+        for i in range(Ke):
+            e2e_step(i)
+        t1.record(s_out)
         barrier()
-        ems = max_over_ranks(e0.elapsed_time(e1)) / Ke
+        ems = max_over_ranks(t0.elapsed_time(t1)) / Ke
+        ok_e2e = bool(torch.equal(hz[(Ke - 1) % 2], z.data.cpu()))
         e2e = {"value": FLOP_FWDINV / (ems * 1e-3) / 1e9, "unit": UNIT,
                "ms_per_step": ems, "h2d_bytes_per_step": hx.numel() * 16,
-               "d2h_bytes_per_step": hz.numel() * 16}
+               "d2h_bytes_per_step": hz[0].numel() * 16,
+               "api": "paper_1506_07933_b200.execute (plan/execute through the C ABI)",
+               "result_matches_device_run": ok_e2e}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and os.path.exists(REF_BIN):

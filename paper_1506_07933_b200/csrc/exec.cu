@@ -58,6 +58,25 @@ struct DeviceGuard {
   }
 };
 
+// Internal (exchange / work) buffers keep the reference's axis order but pad
+// the innermost extent so every row starts on a 16-byte boundary (fp32
+// complex rows of odd length, e.g. the 129-bin R2C axis), which lets the TMA
+// path describe them.  User-visible buffers are never padded.
+static int64_t inner_pad(int64_t len, int prec) { return prec == 4 ? (len + 1) & ~int64_t(1) : len; }
+
+static int64_t max_internal_count(const Dist& d, int prec) {
+  int64_t m = 0;
+  if (d.ndim() == 0) return 0;  // unused side of a LocalTranspose stage
+  for (int r = 0; r < d.nranks(); ++r) {
+    int64_t off[kMaxDims], len[kMaxDims];
+    d.extents_of(r, off, len);
+    int64_t n = inner_pad(len[d.ndim() - 1], prec);
+    for (int a = 0; a + 1 < d.ndim(); ++a) n *= len[a];
+    m = std::max(m, n);
+  }
+  return m;
+}
+
 // Bytes of the largest complex block any rank holds in any layout of the
 // plan family (forward and backward of the same geometry), so one context
 // serves execute(bwd, execute(fwd, x, ctx), ctx) as in test_plan.cpp:116-133.
@@ -70,8 +89,8 @@ static size_t family_bytes(const Plan& plan) {
     Plan p = build_plan(plan.dims, plan.decomp, plan.grid, d == 0 ? kf : kb, d, plan.prec, o);
     for (const auto& st : p.stages) {
       if (st.type == StageType::Normalize) continue;
-      m = std::max(m, st.before.max_local_count());
-      if (st.type != StageType::LocalTranspose || true) m = std::max(m, st.after.max_local_count());
+      m = std::max(m, max_internal_count(st.before, plan.prec));
+      m = std::max(m, max_internal_count(st.after, plan.prec));
     }
   }
   return (size_t)m * 2 * plan.prec;
@@ -230,9 +249,13 @@ struct Op {
   std::vector<int> members;
 };
 
-static void row_major_strides(const int64_t* len, int nd, int64_t* st) {
+// Row-major element strides of a block; internal buffers pad the innermost
+// extent (inner_pad).
+static void row_major_strides(const int64_t* len, int nd, int64_t* st, bool internal = false,
+                              int prec = 8) {
   st[nd - 1] = 1;
-  for (int a = nd - 2; a >= 0; --a) st[a] = st[a + 1] * len[a + 1];
+  for (int a = nd - 2; a >= 0; --a)
+    st[a] = st[a + 1] * (a + 1 == nd - 1 && internal ? inner_pad(len[a + 1], prec) : len[a + 1]);
 }
 
 static std::vector<int> group_members(const Dist& d, int me, int g) {
@@ -377,6 +400,7 @@ static std::vector<Op> lower(const Plan& plan, const Ctx& ctx, const void* d_in,
   std::vector<Op> prog;
   const int me = ctx.rank;
   const void* cur = d_in;
+  bool cur_internal = false;  // d_in has the user layout; exch/work are padded
   int slot = 0;
   const auto& S = plan.stages;
   size_t i = 0;
@@ -391,7 +415,7 @@ static std::vector<Op> lower(const Plan& plan, const Ctx& ctx, const void* d_in,
     const int nd = Lb.ndim();
     int64_t offb[kMaxDims], lenb[kMaxDims], sb[kMaxDims];
     Lb.extents_of(me, offb, lenb);
-    row_major_strides(lenb, nd, sb);
+    row_major_strides(lenb, nd, sb, cur_internal, ctx.prec);
     const int v = st.axis;
     int ax_a = -1, ax_b = -1;
     for (int a = 0; a < nd; ++a) {
@@ -433,7 +457,7 @@ static std::vector<Op> lower(const Plan& plan, const Ctx& ctx, const void* d_in,
         const int rq = op.members[q];
         int64_t offo[kMaxDims], leno[kMaxDims], so[kMaxDims];
         Lo.extents_of(rq, offo, leno);
-        row_major_strides(leno, nd, so);
+        row_major_strides(leno, nd, so, true, ctx.prec);
         Dest& d = p.dest[q];
         d.ptr = ctx.exch(rq, slot, parity);
         d.base = offb[u] * so[u];
@@ -450,13 +474,14 @@ static std::vector<Op> lower(const Plan& plan, const Ctx& ctx, const void* d_in,
       b.members = op.members;
       if (b.members.size() > 1) prog.push_back(b);
       cur = ctx.exch(me, slot, parity);
+      cur_internal = true;
       ++slot;
       i += tr->transposed ? 3 : 2;  // the LocalTransposeStage is folded in
     } else {
       const Dist& Lo = st.after;
       int64_t offo[kMaxDims], leno[kMaxDims], so[kMaxDims];
       Lo.extents_of(me, offo, leno);
-      row_major_strides(leno, nd, so);
+      row_major_strides(leno, nd, so, !last_fft, ctx.prec);
       void* out = last_fft ? d_out : ctx.work;
       p.ndest = 1;
       p.oblk = p.n_out > 0 ? p.n_out : 1;
@@ -470,6 +495,7 @@ static std::vector<Op> lower(const Plan& plan, const Ctx& ctx, const void* d_in,
       op.tma = plan_tma(op, ctx.prec);
       prog.push_back(op);
       cur = out;
+      cur_internal = !last_fft;
       i += nm ? 2 : 1;
     }
   }

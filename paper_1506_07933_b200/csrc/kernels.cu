@@ -78,7 +78,10 @@ static cudaError_t launch_prec(int n, const PassParams& p, bool adj, cudaStream_
 // TMA variant: one persistent CTA per SM, 512 threads, STAGES-deep prefetch
 template <typename T, int N>
 struct TmaCfg {
-  static constexpr int EPREF = 8;
+  // fp32 long lanes use 16 elements per thread (radix-16 stages): half the
+  // threads per lane, so twice the adjacent lanes per CTA and 64-128 byte
+  // TMA rows instead of 16-32 (fp64 tiles are bounded by shared memory)
+  static constexpr int EPREF = (sizeof(T) == 4 && N >= 512) ? 16 : 8;
   using SC = Sched<N, EPREF>;
   static constexpr int TPL = SC::TPL;
   static constexpr int W0 = DFFTB_TMA_THREADS / TPL;

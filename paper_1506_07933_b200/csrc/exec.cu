@@ -363,8 +363,10 @@ static bool plan_tma(Op& op, int prec) {
   }
   const int64_t lane_elems = p.in_mode == kInHermitian ? n / 2 + 1 : n;
   const int esize = p.in_mode == kInReal ? prec : csize;
-  const int64_t lane_bytes = lane_elems * esize;
-  if (p.in_sb != lane_elems || lane_bytes % 16) return false;
+  // lanes are adjacent rows (row stride in_sb >= lane length: internal
+  // buffers pad odd fp32 rows); W rows go in one bulk copy, padding included
+  const int64_t lane_bytes = p.in_sb * esize;
+  if (p.in_sb < lane_elems || p.in_sb > n || lane_bytes % 16) return false;
   if (p.A > 1 && (p.in_sa * esize) % 16) return false;
   tp.args.bulk = 1;
   tp.args.lane_bytes = (int)lane_bytes;

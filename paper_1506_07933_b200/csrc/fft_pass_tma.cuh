@@ -232,6 +232,7 @@ __global__ void __launch_bounds__(W* Sched<N, EPREF>::TPL, DFFTB_TMA_MINB)
     }
   }
 
+  T lmax = T(0), limag = T(0);  // C2R statistics, reduced once per CTA at the end
   int k = 0;
   for (int64_t t = blockIdx.x; t < ta.ntiles; t += gridDim.x, ++k) {
     const int s = k % STAGES;
@@ -254,18 +255,16 @@ __global__ void __launch_bounds__(W* Sched<N, EPREF>::TPL, DFFTB_TMA_MINB)
     if constexpr (LK == kC2R) {
       // NonHermitian statistics straight from the staged half spectrum:
       // block max |X| and the DC / Nyquist imaginary residues of active lanes
-      T lmax = T(0), limag = T(0);
       if (beta < p.B) {
         const int ll = ta.lane_bytes / ESIZE;
         const C* scp = reinterpret_cast<const C*>(st) + w * ll;
-        for (int i = j; i < ll; i += TPL) {
+        for (int i = j; i <= N / 2; i += TPL) {  // stored bins only, not the row padding
           const C x = scp[i];
           const T m = sqrt(x.x * x.x + x.y * x.y);
           lmax = m > lmax ? m : lmax;
           if (i == 0 || i == N / 2) limag = fabs(x.y) > limag ? fabs(x.y) : limag;
         }
       }
-      herm_reduce<T>(p.herm, lmax, limag);
     }
     __syncthreads();  // staging slot s fully consumed by every thread
     if (tid == 0) {
@@ -278,6 +277,7 @@ __global__ void __launch_bounds__(W* Sched<N, EPREF>::TPL, DFFTB_TMA_MINB)
     run_stages<T, N, EPREF, 0>(v, lane, tw, j);
     if (beta < p.B) store_lk<T, N, EPREF, LK>(p, sptr, v, j, alpha, beta, sc);
   }
+  if constexpr (LK == kC2R) herm_reduce<T>(p.herm, lmax, limag);
 }
 
 }  // namespace dfftb

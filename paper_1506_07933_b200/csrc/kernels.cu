@@ -19,7 +19,7 @@ void count_launch() { g_launches.fetch_add(1); }
 // Stockham), TPL = N/E threads per lane, W lanes per CTA, <= 512 threads.
 template <typename T, int N>
 struct PassCfg {
-  static constexpr int EPREF = 8;
+  static constexpr int EPREF = (sizeof(T) == 4 && N >= 256) ? 16 : 8;
   using SC = Sched<N, EPREF>;
   static constexpr int TPL = SC::TPL;
 #ifndef DFFTB_THREADS
@@ -81,7 +81,7 @@ struct TmaCfg {
   // fp32 long lanes use 16 elements per thread (radix-16 stages): half the
   // threads per lane, so twice the adjacent lanes per CTA and 64-128 byte
   // TMA rows instead of 16-32 (fp64 tiles are bounded by shared memory)
-  static constexpr int EPREF = (sizeof(T) == 4 && N >= 512) ? 16 : 8;
+  static constexpr int EPREF = (sizeof(T) == 4 && N >= 256) ? 16 : 8;
   using SC = Sched<N, EPREF>;
   static constexpr int TPL = SC::TPL;
   static constexpr int W0 = DFFTB_TMA_THREADS / TPL;

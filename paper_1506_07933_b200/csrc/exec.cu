@@ -18,6 +18,7 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <complex>
 #include <cmath>
 #include <cstring>
 #include <vector>
@@ -96,15 +97,101 @@ static size_t family_bytes(const Plan& plan) {
   return (size_t)m * 2 * plan.prec;
 }
 
+static bool is_pow2(int64_t n) { return n >= 1 && (n & (n - 1)) == 0; }
+
+static int64_t largest_prime_factor(int64_t n) {
+  int64_t lpf = 1;
+  for (int64_t p = 2; p * p <= n; ++p)
+    while (n % p == 0) {
+      lpf = p;
+      n /= p;
+    }
+  return n > 1 ? std::max(lpf, n) : lpf;
+}
+
+// Kernel1d path choice (kernels.hpp:227-243): pow-2 -> Stockham pass,
+// 13-smooth -> mixed radix, else Bluestein with m = bit_ceil(2n - 1)
+static bool is_smooth(int64_t n) { return largest_prime_factor(n) <= 13; }
+static int64_t bluestein_m(int64_t n) {
+  int64_t m = 1;
+  while (m < 2 * n - 1) m <<= 1;
+  return m;
+}
+
+static std::vector<int> radix_list(int64_t L) {
+  std::vector<int> r;
+  while (L % 8 == 0) { r.push_back(8); L /= 8; }
+  while (L % 4 == 0) { r.push_back(4); L /= 4; }
+  while (L % 2 == 0) { r.push_back(2); L /= 2; }
+  for (int p : {3, 5, 7, 11, 13})
+    while (L % p == 0) { r.push_back(p); L /= p; }
+  return r;
+}
+
 static void check_lengths(const Plan& plan) {
   if (plan.dims.size() != 3 && plan.dims.size() != 2)
     raise(DFFTB_Unsupported, "the B200 path executes 2-D and 3-D transforms");
-  for (auto n : plan.dims)
-    if (!pass_length_supported(n))
+  for (auto n : plan.dims) {
+    bool ok = n >= 1 && n <= 4096;
+    if (ok && !is_pow2(n) && !is_smooth(n)) ok = bluestein_m(n) <= (plan.prec == 8 ? 4096 : 8192);
+    if (!ok)
       raise(DFFTB_Unsupported, "axis length " + std::to_string(n) +
-                                   " not supported on the B200 path (powers of two <= 4096)");
+                                   " not supported on the B200 path (<= 4096; Bluestein <= " +
+                                   std::to_string(plan.prec == 8 ? 2048 : 4096) + ")");
+  }
   for (int g : plan.grid)
     if (g > kMaxDest) raise(DFFTB_Unsupported, "grid factors above 8 are not supported");
+}
+
+// host FFT (recursive radix-2, double) for the Bluestein kernel spectrum
+static void host_fft(std::vector<std::complex<double>>& a) {
+  const size_t n = a.size();
+  if (n <= 1) return;
+  std::vector<std::complex<double>> e(n / 2), o(n / 2);
+  for (size_t i = 0; i < n / 2; ++i) {
+    e[i] = a[2 * i];
+    o[i] = a[2 * i + 1];
+  }
+  host_fft(e);
+  host_fft(o);
+  for (size_t k = 0; k < n / 2; ++k) {
+    const std::complex<double> t = std::polar(1.0, -2.0 * M_PI * (double)k / (double)n) * o[k];
+    a[k] = e[k] + t;
+    a[k + n / 2] = e[k] - t;
+  }
+}
+
+// Bluestein tables for the forward direction (bluestein_context,
+// kernels.hpp:179-216): chirp c_j = exp(-i pi (j^2 mod 2n) / n) and the
+// kernel spectrum FFT_m(wrapped conj(c)) / m, in double, cast to T
+static std::pair<void*, void*> bluestein_tables(int64_t n, int prec) {
+  const int64_t m = bluestein_m(n);
+  std::vector<std::complex<double>> chirp(n), b(m, 0.0);
+  for (int64_t j = 0; j < n; ++j) {
+    const uint64_t r = ((uint64_t)j * (uint64_t)j) % (uint64_t)(2 * n);
+    chirp[j] = std::polar(1.0, -M_PI * (double)r / (double)n);
+  }
+  b[0] = std::conj(chirp[0]);
+  for (int64_t j = 1; j < n; ++j) b[j] = b[m - j] = std::conj(chirp[j]);
+  host_fft(b);
+  for (auto& v : b) v /= (double)m;
+  auto upload = [&](const std::vector<std::complex<double>>& v) {
+    void* d = nullptr;
+    if (prec == 8) {
+      CUDA_TRY(cudaMalloc(&d, v.size() * 16));
+      CUDA_TRY(cudaMemcpy(d, v.data(), v.size() * 16, cudaMemcpyHostToDevice));
+    } else {
+      std::vector<float> f(2 * v.size());
+      for (size_t i = 0; i < v.size(); ++i) {
+        f[2 * i] = (float)v[i].real();
+        f[2 * i + 1] = (float)v[i].imag();
+      }
+      CUDA_TRY(cudaMalloc(&d, f.size() * 4));
+      CUDA_TRY(cudaMemcpy(d, f.data(), f.size() * 4, cudaMemcpyHostToDevice));
+    }
+    return d;
+  };
+  return {upload(chirp), upload(b)};
 }
 
 Ctx* ctx_create(const Plan& plan, int rank, int device) {
@@ -135,7 +222,8 @@ Ctx* ctx_create(const Plan& plan, int rank, int device) {
   // (TwiddleTable, kernels.hpp:66-98); forward only: backward is conj(F(conj x))
   for (auto n64 : plan.dims) {
     const int n = (int)n64;
-    if (ctx->twiddles.count(n)) continue;
+    if (!is_pow2(n) && !is_smooth(n) && !ctx->bluestein.count(n)) ctx->bluestein[n] = bluestein_tables(n, plan.prec);
+    if (!is_pow2(n) || ctx->twiddles.count(n)) continue;
     std::vector<double> wd(2 * n);
     std::vector<float> wf(2 * n);
     for (int m = 0; m < n; ++m) {
@@ -210,6 +298,10 @@ void ctx_destroy(Ctx* ctx) {
     for (int r = 0; r < ctx->nranks; ++r)
       if (ctx->peer_opened[r]) cudaIpcCloseMemHandle(ctx->peer_region[r]);
     for (auto& kv : ctx->twiddles) cudaFree(kv.second);
+    for (auto& kv : ctx->bluestein) {
+      cudaFree(kv.second.first);
+      cudaFree(kv.second.second);
+    }
     cudaFree(ctx->region);
     cudaFree(ctx->work);
     cudaFree(ctx->dstat);
@@ -240,6 +332,8 @@ void world_create(const Plan& plan, int device, Ctx** out) {
 struct Op {
   bool barrier = false;
   bool tma = false;
+  bool generic = false;  // non-power-of-two length: mixed-radix / Bluestein kernel
+  GenParams g{};
   TmaPlan tp{};
   PassParams p{};
   int n = 1;
@@ -327,6 +421,15 @@ static bool plan_tma(Op& op, int prec) {
     if ((2 * W * prec) % 16 != 0 || 2 * W > 256) return false;
     const int64_t si = p.in_si * csize, sa = (p.A > 1 ? p.in_sa : (int64_t)n * p.in_si) * csize;
     if (si % 16 || sa % 16 || (p.in_sb != 1)) return false;
+    tp.args.bulk = 0;
+    {
+      // row loader: TMA boxes (default; measured faster even for 4-16 MB row
+      // strides) or per-thread cp.async (DFFTB_ADJ_LOADER=ldgsts|auto)
+      const char* e = getenv("DFFTB_ADJ_LOADER");
+      const std::string mode = e ? e : "tma";
+      tp.args.ldgsts = mode == "ldgsts" || (mode == "auto" && si >= (int64_t(1) << 20));
+      if (tp.args.ldgsts) return true;
+    }
     auto enc = tensor_map_encoder();
     if (!enc) return false;
     const int rows = n < 256 ? n : 256;
@@ -395,6 +498,30 @@ static void set_store_mode(PassParams& p) {
   p.omask = (int)b - 1;
 }
 
+// Non-power-of-two lengths run the generic mixed-radix / Bluestein kernel
+static void plan_generic(Op& op, const Ctx& ctx) {
+  if (is_pow2(op.n)) return;
+  op.tma = false;
+  op.generic = true;
+  GenParams& g = op.g;
+  std::memset(&g, 0, sizeof(g));
+  g.p = op.p;
+  g.n = op.n;
+  g.bluestein = !is_smooth(op.n);
+  g.L = g.bluestein ? (int)bluestein_m(op.n) : op.n;
+  const auto rl = radix_list(g.L);
+  g.nrad = (int)rl.size();
+  for (int i = 0; i < g.nrad; ++i) g.rad[i] = rl[i];
+  const int64_t csize = 2 * ctx.prec;
+  g.W = (int)std::max<int64_t>(1, std::min<int64_t>(64, 65536 / (g.L * csize)));
+  if (g.bluestein) {
+    g.chirp = ctx.bluestein.at(op.n).first;
+    g.kfft = ctx.bluestein.at(op.n).second;
+  }
+  // the generic store maps (lane, k) by dest contiguity; one dest or general
+  g.p.store_mode = 2;
+}
+
 // One rank's program: fused passes and barriers.  `peer` supplies the
 // exchange-buffer base of any world rank (its own mapping of the peers).
 static std::vector<Op> lower(const Plan& plan, const Ctx& ctx, const void* d_in, void* d_out,
@@ -440,7 +567,7 @@ static std::vector<Op> lower(const Plan& plan, const Ctx& ctx, const void* d_in,
     p.out_real = st.fkind == DFFTB_C2R;
     p.inverse = st.dir == DFFTB_BACKWARD;
     p.scale = nm ? nm->factor : 1.0;
-    p.tw = ctx.twiddles.at(n);
+    p.tw = is_pow2(n) ? ctx.twiddles.at(n) : nullptr;
     p.herm = ctx.dstat;
     op.adj = p.in_si != 1;
     if (lenb[v] == 0 && st.fkind != DFFTB_C2R) p.A = 0;
@@ -469,6 +596,7 @@ static std::vector<Op> lower(const Plan& plan, const Ctx& ctx, const void* d_in,
       }
       set_store_mode(p);
       op.tma = plan_tma(op, ctx.prec);
+      plan_generic(op, ctx);
       prog.push_back(op);
       Op b;
       b.barrier = true;
@@ -495,6 +623,7 @@ static std::vector<Op> lower(const Plan& plan, const Ctx& ctx, const void* d_in,
       d.sk = so[v];
       set_store_mode(p);
       op.tma = plan_tma(op, ctx.prec);
+      plan_generic(op, ctx);
       prog.push_back(op);
       cur = out;
       cur_internal = !last_fft;
@@ -522,7 +651,8 @@ static void launch_op(const Ctx& ctx, const Op& op, uint64_t epoch, cudaStream_t
     return;
   }
   if ((int64_t)op.p.A * op.p.B == 0) return;
-  if (op.tma) CUDA_TRY(launch_pass_tma(ctx.prec, op.n, op.p, op.adj, op.tp, s));
+  if (op.generic) CUDA_TRY(launch_generic(ctx.prec, op.g, s));
+  else if (op.tma) CUDA_TRY(launch_pass_tma(ctx.prec, op.n, op.p, op.adj, op.tp, s));
   else CUDA_TRY(launch_pass(ctx.prec, op.n, op.p, op.adj, s));
 }
 

@@ -26,6 +26,7 @@ struct TmaArgs {
   int rows;        // box rows per TMA op (ADJ)
   int bulk;        // 1: contiguous cp.async.bulk, 0: tensor map
   int lane_bytes;  // bulk mode: bytes of one stored lane
+  int ldgsts;      // strided lanes: per-thread cp.async (16 B) instead of TMA boxes
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -198,10 +199,29 @@ __global__ void __launch_bounds__(W* Sched<N, EPREF>::TPL, DFFTB_TMA_MINB)
   constexpr int ESIZE = LK == kR2C ? (int)sizeof(T) : (int)sizeof(C);
   const T sc = static_cast<T>(p.scale);
 
+  // called by every thread; TMA ops are issued by thread 0 only
   auto issue = [&](int64_t t, int s) {
     const int alpha = (int)(t / tiles_b);
     const int beta0 = (int)(t - (int64_t)alpha * tiles_b) * W;
     unsigned char* dst = stg + s * TL::STG;
+    if (ADJ && ta.ldgsts) {
+      // very large row strides (e.g. the axis-0 pass) translate one page per
+      // row: spread the rows over all threads' LSU path instead of one TMA
+      // box walk.  Tile layout [i][w] as for TMA; lanes past B read as zero.
+      const C* src0 = reinterpret_cast<const C*>(p.in) + (int64_t)alpha * p.in_sa;
+      constexpr int NT = W * TPL;
+      for (int e = tid; e < W * N; e += NT) {
+        const int i = e / W, ww = e - (e / W) * W;
+        const bool ok = beta0 + ww < p.B;
+        const C* src = src0 + (int64_t)(ok ? beta0 + ww : 0) * p.in_sb + (int64_t)i * p.in_si;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst + (size_t)e * sizeof(C))),
+                     "l"(src), "r"(ok ? 16 : 0)
+                     : "memory");
+      }
+      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&bars[s])) : "memory");
+      return;
+    }
+    if (tid != 0) return;
     if constexpr (ADJ) {
       mbar_expect_tx(&bars[s], (uint32_t)(W * N * sizeof(C)));
       for (int r0 = 0; r0 < N; r0 += ta.rows) {
@@ -220,16 +240,14 @@ __global__ void __launch_bounds__(W* Sched<N, EPREF>::TPL, DFFTB_TMA_MINB)
   };
 
   if (tid == 0) {
-    for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], (ADJ && ta.ldgsts) ? W * TPL : 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (tid < kMaxDest) sptr[tid] = p.dest[tid].ptr;
   __syncthreads();
-  if (tid == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      const int64_t t = blockIdx.x + (int64_t)s * gridDim.x;
-      if (t < ta.ntiles) issue(t, s);
-    }
+  for (int s = 0; s < STAGES; ++s) {
+    const int64_t t = blockIdx.x + (int64_t)s * gridDim.x;
+    if (t < ta.ntiles) issue(t, s);
   }
 
   T lmax = T(0), limag = T(0);  // C2R statistics, reduced once per CTA at the end
@@ -267,7 +285,7 @@ __global__ void __launch_bounds__(W* Sched<N, EPREF>::TPL, DFFTB_TMA_MINB)
       }
     }
     __syncthreads();  // staging slot s fully consumed by every thread
-    if (tid == 0) {
+    {
       const int64_t t2 = t + (int64_t)STAGES * gridDim.x;
       if (t2 < ta.ntiles) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

@@ -126,6 +126,7 @@ struct Ctx {
   size_t work_bytes = 0;
   unsigned long long* dstat = nullptr;  // [0] herm max, [1] herm imag, [2] timeout flag, [3] nonfinite
   std::map<int, void*> twiddles;        // N -> device table (prec of the ctx)
+  std::map<int, std::pair<void*, void*>> bluestein;  // n -> (chirp, kernel spectrum)
 
   std::vector<void*> peer_region;  // per world rank, mapped into this process
   std::vector<bool> peer_opened;   // opened through cudaIpcOpenMemHandle

@@ -4,6 +4,7 @@
 #include <cstdio>
 
 #include "fft_pass.cuh"
+#include "fft_generic.cuh"
 #include "fft_pass_tma.cuh"
 #include "kernels.hpp"
 
@@ -171,6 +172,27 @@ int tma_tile_w(int prec, int n) { return prec == 8 ? tma_w_prec<double>(n) : tma
 cudaError_t launch_pass_tma(int prec, int n, const PassParams& p, bool adj, const TmaPlan& tp,
                             cudaStream_t s) {
   return prec == 8 ? launch_tma_prec<double>(n, p, adj, tp, s) : launch_tma_prec<float>(n, p, adj, tp, s);
+}
+
+// ------------------------------------------------------- generic lengths
+
+cudaError_t launch_generic(int prec, const GenParams& g, cudaStream_t s) {
+  const int64_t tiles = (int64_t)g.p.A * ((g.p.B + g.W - 1) / g.W);
+  if (tiles <= 0) return cudaSuccess;
+  const size_t csize = 2 * (size_t)prec;
+  const int smem = (int)(2 * (size_t)g.W * g.L * csize);
+  cudaError_t e;
+  if (prec == 8) {
+    e = cudaFuncSetAttribute(fft_generic_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    fft_generic_kernel<double><<<(unsigned)tiles, 256, smem, s>>>(g);
+  } else {
+    e = cudaFuncSetAttribute(fft_generic_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    fft_generic_kernel<float><<<(unsigned)tiles, 256, smem, s>>>(g);
+  }
+  count_launch();
+  return cudaGetLastError();
 }
 
 bool pass_length_supported(int64_t n) {

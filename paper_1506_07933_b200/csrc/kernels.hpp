@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "fft_generic.cuh"
 #include "fft_pass.cuh"
 #include "fft_pass_tma.cuh"
 
@@ -40,6 +41,7 @@ int tma_tile_w(int prec, int n);  // lanes per CTA of the TMA kernel
 cudaError_t launch_pass_tma(int prec, int n, const PassParams& p, bool adj, const TmaPlan& tp,
                             cudaStream_t s);
 cudaError_t launch_pass(int prec, int n, const PassParams& p, bool adj, cudaStream_t s);
+cudaError_t launch_generic(int prec, const GenParams& g, cudaStream_t s);
 cudaError_t launch_barrier(const BarrierParams& bp, cudaStream_t s);
 cudaError_t launch_seeded(int prec, const SeedParams& sp, void* out, cudaStream_t s);
 cudaError_t launch_nonfinite(int prec, const void* x, int64_t n_reals, unsigned long long* count,

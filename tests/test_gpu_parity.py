@@ -18,7 +18,7 @@ from gpu_util import gather, is_pow2, make_plan, rel_l2, run_world, scatter
 pytestmark = pytest.mark.gpu
 
 TOL = {"f64": 1e-12, "f32": 1e-5}
-POW2_CASES = [c for c in O.golden_cases() if all(is_pow2(d) for d in c["dims"])]
+POW2_CASES = O.golden_cases()  # all reference goldens, incl. non-power-of-two lengths
 
 
 @pytest.fixture(autouse=True)
@@ -159,9 +159,38 @@ def test_validate_finite_is_opt_in():
 
 
 def test_unsupported_length_fails_loudly():
-    plan = make_plan("pencil", [6, 6, 6], [1, 1], "c2c", "forward")
+    # prime 2053: Bluestein would need a 8192-point fp64 convolution per lane
+    plan = make_plan("pencil", [2053, 2, 2], [1, 1], "c2c", "forward")
     with pytest.raises(D.Error, match="Unsupported"):
         D.make_context(plan)
+    plan = make_plan("pencil", [8192, 2, 2], [1, 1], "c2c", "forward")
+    with pytest.raises(D.Error, match="Unsupported"):
+        D.make_context(plan)
+
+
+GENERIC_CASES = [
+    # non-power-of-two lengths: mixed radix (13-smooth) and Bluestein (kernels.hpp:143-293)
+    ("pencil", [6, 6, 6], [3, 2], "c2c", "f64"),        # test_plan.cpp:276-281
+    ("pencil", [5, 5, 5], [1, 4], "c2c", "f64"),        # empty tails
+    ("slab", [17, 4, 4], [3], "c2c", "f64"),            # prime -> Bluestein
+    ("slab", [12, 10, 12], [4], "c2c", "f64"),
+    ("pencil", [8, 8, 7], [2, 2], "r2c", "f64"),        # odd last axis
+    ("pencil", [8, 4, 6], [2, 2], "r2c", "f64"),
+    ("pencil", [30, 18, 20], [2, 3], "r2c", "f32"),
+    ("slab", [96, 120, 64], [4], "c2c", "f64"),
+    ("pencil", [2, 3, 1000], [1, 1], "r2c", "f64"),     # 1000 = 8*125
+    ("pencil", [4, 2, 1021], [1, 1], "c2c", "f64"),     # prime 1021 -> Bluestein m=2048
+    ("pencil", [3, 2, 509], [1, 1], "r2c", "f32"),      # prime R2C/C2R fp32
+    ("slab", [11, 13, 6], [2], "c2c", "f32"),
+]
+
+
+@pytest.mark.parametrize("decomp,dims,grid,kind,prec", GENERIC_CASES,
+                         ids=["-".join(map(str, [c[0], "x".join(map(str, c[1])),
+                                                 "x".join(map(str, c[2])), c[3], c[4]]))
+                              for c in GENERIC_CASES])
+def test_generic_lengths_against_oracle(decomp, dims, grid, kind, prec):
+    test_against_oracle(decomp, dims, grid, kind, prec)
 
 
 def test_context_reused_for_forward_and_backward():

@@ -125,6 +125,10 @@ struct Ctx {
   void* work = nullptr;  // private scratch for local->local passes
   size_t work_bytes = 0;
   unsigned long long* dstat = nullptr;  // [0] herm max, [1] herm imag, [2] timeout flag, [3] nonfinite
+  void* fuse_ring = nullptr;            // L2-resident plane ring of the fused two-axis pass
+  size_t fuse_ring_bytes = 0;
+  unsigned int* fuse_counters = nullptr;  // [2 * fuse_planes]
+  int fuse_planes = 0;
   std::map<int, void*> twiddles;        // N -> device table (prec of the ctx)
   std::map<int, std::pair<void*, void*>> bluestein;  // n -> (chirp, kernel spectrum)
 

@@ -169,6 +169,57 @@ static int tma_w_prec(int n) {
 
 int tma_tile_w(int prec, int n) { return prec == 8 ? tma_w_prec<double>(n) : tma_w_prec<float>(n); }
 
+// ----------------------------------------------- fused two-axis plane pipeline
+
+template <typename T, int N, bool FWD>
+static cudaError_t launch_fused2_tn(const PassParams& pa, const PassParams& pb, const CUtensorMap& tm,
+                                    const Fused2Args& fa, cudaStream_t s) {
+  using Cf = TmaCfg<T, N>;
+  using TL = TmaLayout<T, N, Cf::W>;
+  constexpr int SMEM = 2 * TL::STG + TL::XCH + 16 + 8 * kMaxDest;
+  auto kern = fft_fused2_kernel<T, N, Cf::EPREF, Cf::W, FWD>;
+  static int grid_cap[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  if (!grid_cap[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    if (e != cudaSuccess) return e;
+    int occ = 0, sms = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Cf::THREADS, SMEM);
+    if (e != cudaSuccess) return e;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    grid_cap[dev] = (occ < 1 ? 1 : occ) * sms;  // all CTAs co-resident (dependency waits)
+  }
+  const int64_t items = (int64_t)(fa.P + fa.lag) * 2 * fa.T;
+  const int64_t grid = items < grid_cap[dev] ? items : grid_cap[dev];
+  kern<<<(unsigned)grid, Cf::THREADS, SMEM, s>>>(pa, pb, tm, fa);
+  count_launch();
+  return cudaGetLastError();
+}
+
+template <typename T>
+static cudaError_t launch_fused2_prec(int n, bool fwd, const PassParams& pa, const PassParams& pb,
+                                      const CUtensorMap& tm, const Fused2Args& fa, cudaStream_t s) {
+  switch (n) {
+    case 64: return fwd ? launch_fused2_tn<T, 64, true>(pa, pb, tm, fa, s) : launch_fused2_tn<T, 64, false>(pa, pb, tm, fa, s);
+    case 128: return fwd ? launch_fused2_tn<T, 128, true>(pa, pb, tm, fa, s) : launch_fused2_tn<T, 128, false>(pa, pb, tm, fa, s);
+    case 256: return fwd ? launch_fused2_tn<T, 256, true>(pa, pb, tm, fa, s) : launch_fused2_tn<T, 256, false>(pa, pb, tm, fa, s);
+    case 512: return fwd ? launch_fused2_tn<T, 512, true>(pa, pb, tm, fa, s) : launch_fused2_tn<T, 512, false>(pa, pb, tm, fa, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+bool fused2_supported(int prec, int n) {
+  return (n == 64 || n == 128 || n == 256 || n == 512) && tma_tile_w(prec, n) > 0;
+}
+
+cudaError_t launch_fused2(int prec, int n, bool fwd, const PassParams& pa, const PassParams& pb,
+                          const CUtensorMap& tm, const Fused2Args& fa, cudaStream_t s) {
+  return prec == 8 ? launch_fused2_prec<double>(n, fwd, pa, pb, tm, fa, s)
+                   : launch_fused2_prec<float>(n, fwd, pa, pb, tm, fa, s);
+}
+
 cudaError_t launch_pass_tma(int prec, int n, const PassParams& p, bool adj, const TmaPlan& tp,
                             cudaStream_t s) {
   return prec == 8 ? launch_tma_prec<double>(n, p, adj, tp, s) : launch_tma_prec<float>(n, p, adj, tp, s);

@@ -7,6 +7,7 @@
 #include "fft_generic.cuh"
 #include "fft_pass.cuh"
 #include "fft_pass_tma.cuh"
+#include "fft_fused2.cuh"
 
 namespace dfftb {
 
@@ -38,6 +39,9 @@ struct TmaPlan {
   TmaArgs args;
 };
 int tma_tile_w(int prec, int n);  // lanes per CTA of the TMA kernel
+bool fused2_supported(int prec, int n);
+cudaError_t launch_fused2(int prec, int n, bool fwd, const PassParams& pa, const PassParams& pb,
+                          const CUtensorMap& tm, const Fused2Args& fa, cudaStream_t s);
 cudaError_t launch_pass_tma(int prec, int n, const PassParams& p, bool adj, const TmaPlan& tp,
                             cudaStream_t s);
 cudaError_t launch_pass(int prec, int n, const PassParams& p, bool adj, cudaStream_t s);

@@ -190,6 +190,28 @@ const char* dfftb_last_error_message(void);
 /* Number of dfftb kernels launched by this process so far (evidence counter). */
 uint64_t dfftb_kernel_launch_count(void);
 
+/* ---- spectral operators (spectral.hpp:133-309) --------------------------
+ * Applied to this rank's block of a FORWARD plan's output (the frequency
+ * layout; NotFrequencyLayout otherwise), on device:
+ *   DFFTB_SPECTRAL_DERIV         out (+)= i k_axis (.) in, Nyquist mode zeroed
+ *                                (axis_k_deriv, spectral.hpp:24-56, 131-164)
+ *   DFFTB_SPECTRAL_LAPLACIAN     out (+)= -|k|^2 (.) in        (:219-249)
+ *   DFFTB_SPECTRAL_INV_LAPLACIAN out (+)= in / -|k|^2, k = 0 pinned to 0; the
+ *                                owner of the k = 0 bin checks |in(0)| <= 1e-12 N
+ *                                and returns NonZeroMean otherwise (:255-309)
+ * k_a = 2 pi / L_a * signed index (R2C half axis: non-negative).
+ * domain_lengths: ndim values (NULL = 2 pi each).  accumulate != 0 adds into
+ * out (divergence).  in == out is allowed. */
+enum { DFFTB_SPECTRAL_DERIV = 0, DFFTB_SPECTRAL_LAPLACIAN = 1, DFFTB_SPECTRAL_INV_LAPLACIAN = 2 };
+dfftb_status dfftb_spectral_apply(dfftb_plan forward_plan, int rank, int op, int axis,
+                                  const double* domain_lengths, const void* d_in, void* d_out,
+                                  int accumulate, void* stream);
+/* wavenumbers (spectral.hpp:24-56): the local k values of `axis` for this
+ * rank's frequency block (length = local extent); deriv != 0 gives
+ * axis_k_deriv (Nyquist zeroed), else axis_k. */
+dfftb_status dfftb_wavenumbers(dfftb_plan forward_plan, int rank, int axis, int deriv,
+                               const double* domain_lengths, double* k_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -62,6 +62,10 @@ _SIGS = {
     "dfftb_error_name": (_c.c_char_p, [_c.c_int]),
     "dfftb_last_error_message": (_c.c_char_p, []),
     "dfftb_kernel_launch_count": (_c.c_uint64, []),
+    "dfftb_spectral_apply": (_c.c_int, [vp, _c.c_int, _c.c_int, _c.c_int,
+                                        _c.POINTER(_c.c_double), vp, vp, _c.c_int, vp]),
+    "dfftb_wavenumbers": (_c.c_int, [vp, _c.c_int, _c.c_int, _c.c_int,
+                                     _c.POINTER(_c.c_double), _c.POINTER(_c.c_double)]),
 }
 
 _LIB = None

@@ -262,3 +262,22 @@ const char* dfftb_last_error_message(void) { return g_last_error.c_str(); }
 uint64_t dfftb_kernel_launch_count(void) { return dfftb::launch_count(); }
 
 }  // extern "C"
+
+extern "C" {
+
+dfftb_status dfftb_spectral_apply(dfftb_plan forward_plan, int rank, int op, int axis,
+                                  const double* domain_lengths, const void* d_in, void* d_out,
+                                  int accumulate, void* stream) {
+  return guarded([&] {
+    dfftb::spectral_apply(forward_plan->plan, rank, op, axis, domain_lengths, d_in, d_out, accumulate,
+                          static_cast<cudaStream_t>(stream));
+  });
+}
+
+dfftb_status dfftb_wavenumbers(dfftb_plan forward_plan, int rank, int axis, int deriv,
+                               const double* domain_lengths, double* k_out) {
+  return guarded(
+      [&] { dfftb::wavenumbers(forward_plan->plan, rank, axis, deriv, domain_lengths, k_out); });
+}
+
+}  // extern "C"

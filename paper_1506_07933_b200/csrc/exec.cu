@@ -913,3 +913,72 @@ void fill_seeded(const Plan& plan, int rank, int side, uint64_t seed, int comple
 }
 
 }  // namespace dfftb
+
+namespace dfftb {
+
+// ------------------------------------------------------- spectral operators
+
+static SpectralParams spectral_params(const Plan& plan, int rank, const double* lengths) {
+  if (plan.dir != DFFTB_FORWARD) raise(DFFTB_NotFrequencyLayout, "spectral operators need a forward plan's output layout");
+  const Dist& f = plan.output;  // frequency layout: all hatted, complex
+  if (rank < 0 || rank >= f.nranks()) raise(DFFTB_InvalidRank, "rank out of range");
+  SpectralParams sp{};
+  sp.nd = f.ndim();
+  if (sp.nd > 4) raise(DFFTB_Unsupported, "at most 4 axes");
+  f.extents_of(rank, sp.off, sp.len);
+  sp.count = 1;
+  for (int a = 0; a < sp.nd; ++a) {
+    sp.n[a] = plan.dims[a];
+    sp.half[a] = f.dims[a] != plan.dims[a];
+    sp.scale[a] = 2.0 * M_PI / (lengths ? lengths[a] : 2.0 * M_PI);
+    sp.count *= sp.len[a];
+  }
+  return sp;
+}
+
+void spectral_apply(const Plan& plan, int rank, int op, int axis, const double* lengths, const void* in,
+                    void* out, int accumulate, cudaStream_t s) {
+  SpectralParams sp = spectral_params(plan, rank, lengths);
+  if (op < 0 || op > 2) raise(DFFTB_ConfigInvalid, "unknown spectral operator");
+  if (op == 0 && (axis < 0 || axis >= sp.nd)) raise(DFFTB_OutOfRange, "derivative axis out of range");
+  sp.op = op;
+  sp.axis = op == 0 ? axis : 0;
+  sp.accumulate = accumulate;
+  if (op == 2) {
+    // inverse_laplacian needs a zero-mean field (spectral.hpp:266-281)
+    bool owns_zero = sp.count > 0;
+    for (int a = 0; a < sp.nd; ++a) owns_zero = owns_zero && sp.off[a] == 0;
+    if (owns_zero) {
+      double v[2] = {0, 0};
+      if (plan.prec == 8) {
+        CUDA_TRY(cudaMemcpyAsync(v, in, 16, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+      } else {
+        float fv[2];
+        CUDA_TRY(cudaMemcpyAsync(fv, in, 8, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        v[0] = fv[0];
+        v[1] = fv[1];
+      }
+      double total = 1;
+      for (auto d : plan.dims) total *= (double)d;
+      if (std::hypot(v[0], v[1]) > 1e-12 * total)
+        raise(DFFTB_NonZeroMean, "inverse_laplacian needs a zero-mean field");
+    }
+  }
+  CUDA_TRY(launch_spectral(plan.prec, sp, in, out, s));
+}
+
+void wavenumbers(const Plan& plan, int rank, int axis, int deriv, const double* lengths, double* k_out) {
+  SpectralParams sp = spectral_params(plan, rank, lengths);
+  if (axis < 0 || axis >= sp.nd) raise(DFFTB_OutOfRange, "axis out of range");
+  for (int64_t i = 0; i < sp.len[axis]; ++i) {
+    const int64_t g = sp.off[axis] + i;
+    int64_t k = g;
+    if (!sp.half[axis] && 2 * g >= sp.n[axis]) k = g - sp.n[axis];
+    const bool nyq = sp.n[axis] % 2 == 0 && 2 * std::llabs(k) == sp.n[axis];
+    k_out[i] = (deriv && nyq) ? 0.0 : sp.scale[axis] * (double)k;
+  }
+}
+
+}  // namespace dfftb

@@ -352,6 +352,72 @@ __global__ void nonfinite_kernel(const T* x, int64_t n, unsigned long long* coun
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, c);
 }
 
+// ------------------------------------------------------ spectral operators
+
+// signed wavenumber of global index g on axis a (spectral.hpp:42-53)
+__device__ __forceinline__ double wavenumber(const SpectralParams& sp, int a, int64_t g, bool deriv) {
+  int64_t k = g;
+  if (!sp.half[a] && 2 * g >= sp.n[a]) k = g - sp.n[a];
+  const bool nyq = sp.n[a] % 2 == 0 && 2 * (k < 0 ? -k : k) == sp.n[a];
+  return (deriv && nyq) ? 0.0 : sp.scale[a] * (double)k;
+}
+
+// One read + one write of the spectrum block; k computed per element from
+// the global coordinate (no tables), multipliers in double as the reference.
+template <typename T>
+__global__ void spectral_kernel(SpectralParams sp, const Cpx<T>* in, Cpx<T>* out) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; l < sp.count; l += stride) {
+    int64_t rem = l, g[4];
+    for (int a = sp.nd - 1; a >= 0; --a) {
+      g[a] = sp.off[a] + rem % sp.len[a];
+      rem /= sp.len[a];
+    }
+    const Cpx<T> v = in[l];
+    double re, im;
+    if (sp.op == 0) {  // i k_axis (.) v
+      const double k = wavenumber(sp, sp.axis, g[sp.axis], true);
+      re = -k * (double)v.y;
+      im = k * (double)v.x;
+    } else {
+      double m = 0.0;
+      for (int a = 0; a < sp.nd; ++a) {
+        const double k = wavenumber(sp, a, g[a], false);
+        m += k * k;
+      }
+      if (sp.op == 1) {
+        re = -m * (double)v.x;
+        im = -m * (double)v.y;
+      } else if (m == 0.0) {
+        re = im = 0.0;
+      } else {
+        re = (double)v.x / -m;
+        im = (double)v.y / -m;
+      }
+    }
+    Cpx<T> r{(T)re, (T)im};
+    if (sp.accumulate) {
+      const Cpx<T> o = out[l];
+      r.x += o.x;
+      r.y += o.y;
+    }
+    out[l] = r;
+  }
+}
+
+cudaError_t launch_spectral(int prec, const SpectralParams& sp, const void* in, void* out, cudaStream_t s) {
+  if (sp.count <= 0) return cudaSuccess;
+  const int threads = 256;
+  int64_t blocks = (sp.count + threads - 1) / threads;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (prec == 8)
+    spectral_kernel<double><<<(unsigned)blocks, threads, 0, s>>>(sp, (const double2*)in, (double2*)out);
+  else
+    spectral_kernel<float><<<(unsigned)blocks, threads, 0, s>>>(sp, (const float2*)in, (float2*)out);
+  count_launch();
+  return cudaGetLastError();
+}
+
 cudaError_t launch_nonfinite(int prec, const void* x, int64_t n_reals, unsigned long long* count,
                              cudaStream_t s) {
   if (n_reals <= 0) return cudaSuccess;

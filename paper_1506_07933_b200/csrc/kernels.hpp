@@ -48,6 +48,16 @@ cudaError_t launch_pass(int prec, int n, const PassParams& p, bool adj, cudaStre
 cudaError_t launch_generic(int prec, const GenParams& g, cudaStream_t s);
 cudaError_t launch_barrier(const BarrierParams& bp, cudaStream_t s);
 cudaError_t launch_seeded(int prec, const SeedParams& sp, void* out, cudaStream_t s);
+struct SpectralParams {
+  int nd;
+  int64_t len[4], off[4];  // local frequency block
+  int64_t n[4];            // spatial lengths (full)
+  int half[4];             // axis stored as a half spectrum (R2C last axis)
+  double scale[4];         // 2 pi / L_a
+  int op, axis, accumulate;
+  int64_t count;
+};
+cudaError_t launch_spectral(int prec, const SpectralParams& sp, const void* in, void* out, cudaStream_t s);
 cudaError_t launch_nonfinite(int prec, const void* x, int64_t n_reals, unsigned long long* count,
                              cudaStream_t s);
 uint64_t launch_count();

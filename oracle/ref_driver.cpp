@@ -67,6 +67,7 @@ struct Args {
   std::vector<std::int64_t> dims{64, 64, 64};
   std::vector<std::int64_t> grid{1};
   bool pencil = false;
+  bool general = false;
   bool r2c = false;
   bool f32 = false;
   std::uint64_t seed = 1;
@@ -84,6 +85,10 @@ Plan<T> make_plan(const Args& a, TransformKind kind, Direction dir) {
   if (a.pencil) {
     std::vector<int> g(a.grid.begin(), a.grid.end());
     return plan_pencil<T>(dims, ProcessGrid(g), kind, dir, opt);
+  }
+  if (a.general) {
+    std::vector<int> g(a.grid.begin(), a.grid.end());
+    return plan_general<T>(dims, ProcessGrid(g), kind, dir, opt);
   }
   return plan_slab<T>(dims, static_cast<int>(a.grid[0]), kind, dir, opt);
 }
@@ -260,7 +265,11 @@ int main(int argc, char** argv) {
     };
     if (k == "--dims") a.dims = parse_list(next());
     else if (k == "--grid") a.grid = parse_list(next());
-    else if (k == "--decomp") a.pencil = std::string(next()) == "pencil";
+    else if (k == "--decomp") {
+      const std::string d = next();
+      a.pencil = d == "pencil";
+      a.general = d == "general";
+    }
     else if (k == "--kind") a.r2c = std::string(next()) == "r2c";
     else if (k == "--prec") a.f32 = std::string(next()) == "f32";
     else if (k == "--seed") a.seed = std::stoull(next());

@@ -129,8 +129,8 @@ static std::vector<int> radix_list(int64_t L) {
 }
 
 static void check_lengths(const Plan& plan) {
-  if (plan.dims.size() != 3 && plan.dims.size() != 2)
-    raise(DFFTB_Unsupported, "the B200 path executes 2-D and 3-D transforms");
+  if (plan.dims.size() < 2 || plan.dims.size() > 4)
+    raise(DFFTB_Unsupported, "the B200 path executes 2-D, 3-D and 4-D transforms");
   for (auto n : plan.dims) {
     bool ok = n >= 1 && n <= 4096;
     if (ok && !is_pow2(n) && !is_smooth(n)) ok = bluestein_m(n) <= (plan.prec == 8 ? 4096 : 8192);
@@ -438,9 +438,11 @@ static bool plan_tma(Op& op, int prec) {
   if ((reinterpret_cast<uintptr_t>(p.in) & 15) != 0) return false;
   TmaPlan& tp = op.tp;
   std::memset(&tp, 0, sizeof(tp));
-  tp.args.ntiles = (int64_t)p.A * ((p.B + W - 1) / W);
+  tp.args.ntiles = (int64_t)p.A * (p.A1 > 1 ? p.A1 : 1) * ((p.B + W - 1) / W);
+  if (p.A1 > 1 && (p.in_sa1 * (p.in_mode == kInReal ? prec : csize)) % 16) return false;
   if (op.adj) {
     if (p.in_mode != kInComplex) return false;
+    if (p.A1 > 1) return false;  // 4-D strided lanes: direct kernel (3-D tensor map only)
     if ((2 * W * prec) % 16 != 0 || 2 * W > 256) return false;
     const int64_t si = p.in_si * csize, sa = (p.A > 1 ? p.in_sa : (int64_t)n * p.in_si) * csize;
     if (si % 16 || sa % 16 || (p.in_sb != 1)) return false;
@@ -561,6 +563,7 @@ static void fuse_pairs(std::vector<Op>& prog, const Ctx& ctx) {
     if (pa.in_mode != kInComplex || pb.in_mode != kInComplex || pa.out_real || pb.out_real) continue;
     if (a.n != b.n || !fused2_supported(prec, a.n) || pa.ndest != 1) continue;
     if (pa.dest[0].ptr != pb.in || pa.A != pb.A || pa.B != pb.B || pa.inverse != pb.inverse) continue;
+    if (pa.A1 > 1 || pb.A1 > 1) continue;
     const bool fwd = !pa.inverse;
     if (fwd ? (a.adj || !b.adj) : (!a.adj || b.adj)) continue;
     if (!a.tma || (fwd ? !a.tp.args.bulk : (a.tp.args.bulk || a.tp.args.ldgsts))) continue;
@@ -657,16 +660,22 @@ static std::vector<Op> lower(const Plan& plan, const Ctx& ctx, const void* d_in,
     Lb.extents_of(me, offb, lenb);
     row_major_strides(lenb, nd, sb, cur_internal, ctx.prec);
     const int v = st.axis;
-    int ax_a = -1, ax_b = -1;
-    for (int a = 0; a < nd; ++a) {
-      if (a == v) continue;
-      if (nd == 3 && ax_a < 0) ax_a = a;
-      else ax_b = a;
+    // lane axes in memory order: [ax_a1 (4-D only)] [ax_a] ax_b (innermost)
+    int ax_a1 = -1, ax_a = -1, ax_b = -1;
+    {
+      int lanes[kMaxDims], nl = 0;
+      for (int a = 0; a < nd; ++a)
+        if (a != v) lanes[nl++] = a;
+      ax_b = lanes[nl - 1];
+      if (nl >= 2) ax_a = lanes[nl - 2];
+      if (nl >= 3) ax_a1 = lanes[nl - 3];
     }
     Op op;
     PassParams& p = op.p;
     p.in = cur;
     p.A = ax_a >= 0 ? (int)lenb[ax_a] : 1;
+    p.A1 = ax_a1 >= 0 ? (int)lenb[ax_a1] : 1;
+    p.in_sa1 = ax_a1 >= 0 ? sb[ax_a1] : 0;
     p.B = (int)lenb[ax_b];
     p.in_sa = ax_a >= 0 ? sb[ax_a] : 0;
     p.in_sb = sb[ax_b];
@@ -702,6 +711,7 @@ static std::vector<Op> lower(const Plan& plan, const Ctx& ctx, const void* d_in,
         d.ptr = ctx.exch(rq, slot, parity);
         d.base = offb[u] * so[u];
         d.sa = ax_a >= 0 ? so[ax_a] : 0;
+        d.sa1 = ax_a1 >= 0 ? so[ax_a1] : 0;
         d.sb = so[ax_b];
         d.sk = so[v];
       }
@@ -730,6 +740,7 @@ static std::vector<Op> lower(const Plan& plan, const Ctx& ctx, const void* d_in,
       d.ptr = out;
       d.base = 0;
       d.sa = ax_a >= 0 ? so[ax_a] : 0;
+        d.sa1 = ax_a1 >= 0 ? so[ax_a1] : 0;
       d.sb = so[ax_b];
       d.sk = so[v];
       set_store_mode(p);

@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(256) fft_generic_kernel(const __grid_constant_
     const int beta = beta0 + w;
     C x = C{T(0), T(0)};
     if (beta < p.B) {
-      const int64_t lane = (int64_t)alpha * p.in_sa + (int64_t)beta * p.in_sb;
+      const int64_t lane = in_alpha_off(p, alpha) + (int64_t)beta * p.in_sb;
       if (p.in_mode == kInComplex) {
         x = reinterpret_cast<const C*>(p.in)[lane + (int64_t)i * p.in_si];
       } else if (p.in_mode == kInReal) {
@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(256) fft_generic_kernel(const __grid_constant_
     const int q = p.ndest > 1 ? (int)(k / p.oblk) : 0;
     const int kk = k - (int)(q * p.oblk);
     const Dest& d = p.dest[q];
-    const int64_t off = d.base + (int64_t)alpha * d.sa + (int64_t)beta * d.sb + (int64_t)kk * d.sk;
+    const int64_t off = d.base + dst_alpha_off(p, d, alpha) + (int64_t)beta * d.sb + (int64_t)kk * d.sk;
     C v = r[(size_t)w * L + k];
     if (p.inverse) v.y = -v.y;
     if (p.out_real) {

@@ -67,6 +67,7 @@ constexpr int kMaxDest = 8;
 struct Dest {
   void* ptr;
   int64_t base, sa, sb, sk;
+  int64_t sa1;  // 4-D tensors: stride of the outermost lane axis
 };
 
 enum InMode : int { kInComplex = 0, kInReal = 1, kInHermitian = 2 };
@@ -75,6 +76,8 @@ struct PassParams {
   const void* in;
   int64_t in_sa, in_sb, in_si;  // strides in elements of the input type
   int A, B;                     // lane extents (alpha outer, beta inner)
+  int A1;                       // 4-D: extent of a second, outermost lane axis (<= 1: none)
+  int64_t in_sa1;               // ... and its input stride
   int in_mode;                  // InMode
   int out_real;                 // store Re() only (C2R)
   int inverse;                  // conj on load and store
@@ -88,6 +91,18 @@ struct PassParams {
   unsigned long long* herm;     // C2R: [0] max |X| bits, [1] max |Im DC/Nyq| bits
   Dest dest[kMaxDest];
 };
+
+// combined outer lane index alpha = a1 * A + a2 (a1 only for 4-D tensors)
+__device__ __forceinline__ int64_t in_alpha_off(const PassParams& p, int alpha) {
+  if (p.A1 <= 1) return (int64_t)alpha * p.in_sa;
+  const int a1 = alpha / p.A;
+  return (int64_t)a1 * p.in_sa1 + (int64_t)(alpha - a1 * p.A) * p.in_sa;
+}
+__device__ __forceinline__ int64_t dst_alpha_off(const PassParams& p, const Dest& d, int alpha) {
+  if (p.A1 <= 1) return (int64_t)alpha * d.sa;
+  const int a1 = alpha / p.A;
+  return (int64_t)a1 * d.sa1 + (int64_t)(alpha - a1 * p.A) * d.sa;
+}
 
 // ------------------------------------------------------------ butterflies
 template <typename C, typename T>
@@ -351,7 +366,7 @@ __device__ __forceinline__ void store_out(const PassParams& p, const Cpx<T>* v, 
         kk = k - static_cast<int>(q * p.oblk);
       }
       const Dest& d = p.dest[q];
-      const int64_t off = d.base + (int64_t)alpha * d.sa + (int64_t)beta * d.sb + (int64_t)kk * d.sk;
+      const int64_t off = d.base + dst_alpha_off(p, d, alpha) + (int64_t)beta * d.sb + (int64_t)kk * d.sk;
       C x = v[t * RL + r];
       if (p.inverse) x.y = -x.y;
       if (p.out_real) {
@@ -390,7 +405,7 @@ __global__ void __launch_bounds__(W* Sched<N, EPREF>::TPL, DFFTB_MINB)
   const bool active = beta < p.B;
   C* lane = smem + w * LS;
   const C* tw = reinterpret_cast<const C*>(p.tw);
-  const int64_t lane_off = (int64_t)alpha * p.in_sa + (int64_t)beta * p.in_sb;
+  const int64_t lane_off = in_alpha_off(p, alpha) + (int64_t)beta * p.in_sb;
   C v[SC::E];
   T lmax = T(0), limag = T(0);
   fetch0<T, N, EPREF>(

@@ -139,7 +139,7 @@ __device__ __forceinline__ void store_lk(const PassParams& p, void* const* sptr,
   };
   if (p.store_mode != 2) {
     const Dest& d0 = p.dest[0];
-    const int64_t tile = d0.base + (int64_t)alpha * d0.sa + (int64_t)beta * d0.sb;
+    const int64_t tile = d0.base + dst_alpha_off(p, d0, alpha) + (int64_t)beta * d0.sb;
     const int sk = (int)d0.sk;
 #pragma unroll
     for (int t = 0; t < NBL; ++t) {
@@ -168,7 +168,7 @@ __device__ __forceinline__ void store_lk(const PassParams& p, void* const* sptr,
         const int q = static_cast<int>(k / p.oblk);
         const int kk = k - static_cast<int>(q * p.oblk);
         const Dest& d = p.dest[q];
-        put(d.ptr, d.base + (int64_t)alpha * d.sa + (int64_t)beta * d.sb + (int64_t)kk * d.sk,
+        put(d.ptr, d.base + dst_alpha_off(p, d, alpha) + (int64_t)beta * d.sb + (int64_t)kk * d.sk,
             v[t * RL + r]);
       }
     }
@@ -234,7 +234,7 @@ __global__ void __launch_bounds__(W* Sched<N, EPREF>::TPL, DFFTB_TMA_MINB)
       const uint32_t bytes = (uint32_t)nvalid * (uint32_t)ta.lane_bytes;
       mbar_expect_tx(&bars[s], bytes);
       const unsigned char* src = reinterpret_cast<const unsigned char*>(p.in) +
-                                 ((int64_t)alpha * p.in_sa + (int64_t)beta0 * p.in_sb) * ESIZE;
+                                 (in_alpha_off(p, alpha) + (int64_t)beta0 * p.in_sb) * ESIZE;
       bulk_load(dst, src, bytes, &bars[s]);
     }
   };

@@ -44,7 +44,7 @@ static cudaError_t launch_tn(const PassParams& p, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     attr_done[dev] = true;
   }
-  const int64_t tiles = (int64_t)p.A * ((p.B + Cf::W - 1) / Cf::W);
+  const int64_t tiles = (int64_t)p.A * (p.A1 > 1 ? p.A1 : 1) * ((p.B + Cf::W - 1) / Cf::W);
   if (tiles <= 0) return cudaSuccess;
   kern<<<(unsigned)tiles, Cf::THREADS, Cf::SMEM, s>>>(p);
   count_launch();
@@ -228,7 +228,7 @@ cudaError_t launch_pass_tma(int prec, int n, const PassParams& p, bool adj, cons
 // ------------------------------------------------------- generic lengths
 
 cudaError_t launch_generic(int prec, const GenParams& g, cudaStream_t s) {
-  const int64_t tiles = (int64_t)g.p.A * ((g.p.B + g.W - 1) / g.W);
+  const int64_t tiles = (int64_t)g.p.A * (g.p.A1 > 1 ? g.p.A1 : 1) * ((g.p.B + g.W - 1) / g.W);
   if (tiles <= 0) return cudaSuccess;
   const size_t csize = 2 * (size_t)prec;
   const int smem = (int)(2 * (size_t)g.W * g.L * csize);

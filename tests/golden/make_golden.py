@@ -38,6 +38,10 @@ CASES = [
     ("r2c_8x8x7_pencil2x2_f64", [8, 8, 7], "pencil", [2, 2], "r2c", "f64"),
     ("c2c_17x4x4_slab3_f64", [17, 4, 4], "slab", [3], "c2c", "f64"),
     ("c2c_12x10x12_slab4_f64", [12, 10, 12], "slab", [4], "c2c", "f64"),
+    # general (d-1)-D decomposition of 4-D tensors (plan.hpp:253-262, test_plan.cpp:243-248)
+    ("c2c_8x6x4x4_general2x2x2_f64", [8, 6, 4, 4], "general", [2, 2, 2], "c2c", "f64"),
+    ("r2c_8x8x4x8_general2x2x2_f64", [8, 8, 4, 8], "general", [2, 2, 2], "r2c", "f64"),
+    ("c2c_16x8x8x4_general2x1x2_f32", [16, 8, 8, 4], "general", [2, 1, 2], "c2c", "f32"),
 ]
 
 

@@ -369,10 +369,27 @@ struct Op {
 // Row-major element strides of a block; internal buffers pad the innermost
 // extent (inner_pad).
 static void row_major_strides(const int64_t* len, int nd, int64_t* st, bool internal = false,
-                              int prec = 8) {
-  st[nd - 1] = 1;
-  for (int a = nd - 2; a >= 0; --a)
-    st[a] = st[a + 1] * (a + 1 == nd - 1 && internal ? inner_pad(len[a + 1], prec) : len[a + 1]);
+                              int prec = 8, bool swap01 = false) {
+  // storage order: axes 0,1,2,... outermost first; swap01 stores axis 1
+  // outside axis 0 (the [x1][x0][rest] order of the reference's transposed
+  // pack, exchange.hpp:486-511) so the axis-0 pass reads short strides
+  int order[kMaxDims];
+  for (int a = 0; a < nd; ++a) order[a] = a;
+  if (swap01 && nd >= 3) {
+    order[0] = 1;
+    order[1] = 0;
+  }
+  int64_t s = 1;
+  for (int idx = nd - 1; idx >= 0; --idx) {
+    const int a = order[idx];
+    st[a] = s;
+    s *= (idx == nd - 1 && internal) ? inner_pad(len[a], prec) : len[a];
+  }
+}
+
+static bool zperm_enabled() {
+  const char* e = getenv("DFFTB_ZPERM");
+  return !(e && *e == '0');
 }
 
 static std::vector<int> group_members(const Dist& d, int me, int g) {
@@ -644,6 +661,7 @@ static std::vector<Op> lower(const Plan& plan, const Ctx& ctx, const void* d_in,
   const int me = ctx.rank;
   const void* cur = d_in;
   bool cur_internal = false;  // d_in has the user layout; exch/work are padded
+  bool cur_swap01 = false;    // current buffer stored [x1][x0][rest]
   int slot = 0;
   const auto& S = plan.stages;
   size_t i = 0;
@@ -658,7 +676,7 @@ static std::vector<Op> lower(const Plan& plan, const Ctx& ctx, const void* d_in,
     const int nd = Lb.ndim();
     int64_t offb[kMaxDims], lenb[kMaxDims], sb[kMaxDims];
     Lb.extents_of(me, offb, lenb);
-    row_major_strides(lenb, nd, sb, cur_internal, ctx.prec);
+    row_major_strides(lenb, nd, sb, cur_internal, ctx.prec, cur_swap01);
     const int v = st.axis;
     // lane axes in memory order: [ax_a1 (4-D only)] [ax_a] ax_b (innermost)
     int ax_a1 = -1, ax_a = -1, ax_b = -1;
@@ -697,6 +715,9 @@ static std::vector<Op> lower(const Plan& plan, const Ctx& ctx, const void* d_in,
       const Dist& Lo = tr->after;
       const int g = tr->grid_axis;
       const int u = tr->before.axis_of_grid[g];
+      // the transposed final forward exchange feeds the axis-0 pass: store
+      // its buffer [x1][x0][rest] so axis-0 lanes read short strides
+      const bool swap_out = tr->transposed && zperm_enabled() && nd >= 3;
       op.fused = true;
       op.grid_axis = g;
       op.members = group_members(Lo, me, g);
@@ -706,7 +727,7 @@ static std::vector<Op> lower(const Plan& plan, const Ctx& ctx, const void* d_in,
         const int rq = op.members[q];
         int64_t offo[kMaxDims], leno[kMaxDims], so[kMaxDims];
         Lo.extents_of(rq, offo, leno);
-        row_major_strides(leno, nd, so, true, ctx.prec);
+        row_major_strides(leno, nd, so, true, ctx.prec, swap_out);
         Dest& d = p.dest[q];
         d.ptr = ctx.exch(rq, slot, parity);
         d.base = offb[u] * so[u];
@@ -726,6 +747,7 @@ static std::vector<Op> lower(const Plan& plan, const Ctx& ctx, const void* d_in,
       if (b.members.size() > 1) prog.push_back(b);
       cur = ctx.exch(me, slot, parity);
       cur_internal = true;
+      cur_swap01 = swap_out;
       ++slot;
       i += tr->transposed ? 3 : 2;  // the LocalTransposeStage is folded in
     } else {
@@ -749,6 +771,7 @@ static std::vector<Op> lower(const Plan& plan, const Ctx& ctx, const void* d_in,
       prog.push_back(op);
       cur = out;
       cur_internal = !last_fft;
+      cur_swap01 = false;
       i += nm ? 2 : 1;
     }
   }

@@ -367,6 +367,15 @@ def main():
         p0, p1 = grid
         nvl = 2 * 16 * n_loc * ((p1 - 1) / p1 + (p0 - 1) / p0)
         t_nvl = nvl / 770e9
+        # SURVEY §8(d) convention: nominal 8 TB/s HBM and 900 GB/s NVLink
+        t_nominal = max(2 * 6 * 16 * n_loc / 8.0e12, nvl / 900e9)
+        traffic = None
+        if world == 1:
+            try:
+                with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as f:
+                    traffic = json.load(f)["512^3_c2c_f64_grid1x1"]["dram_bytes_per_pass_avg"]
+            except Exception:
+                traffic = None
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
             "warmup": W, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
@@ -379,11 +388,17 @@ def main():
             "gpu_launches": l_timed,
             "roundtrip_rel_l2": rt_err,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None,
-                         "kernel": "fft_pass_kernel (average over the 6 passes)",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "traffic_source": "profiles/r1_traffic.json (ncu --set full, per pass)"
+                         if traffic else None,
+                         "algorithmic_bytes_per_pass": alg_bytes,
+                         "kernel": "fft_pass_tma_kernel (average over the 6 passes per fwd+inv)",
                          "peak_source": peak_kind,
+                         "step_bound": "nvlink" if t_nvl > t_hbm else "hbm",
                          "step_roofline_ms": 1e3 * max(t_hbm, t_nvl),
-                         "step_frac": 1e3 * max(t_hbm, t_nvl) / ms},
+                         "step_frac": 1e3 * max(t_hbm, t_nvl) / ms,
+                         "step_roofline_ms_nominal_8TBs_900GBs": 1e3 * t_nominal,
+                         "step_frac_nominal": 1e3 * t_nominal / ms},
             "clocks": sampler.summary() if sampler else None,
             "e2e": e2e,
             "cpu_baseline": cpu,

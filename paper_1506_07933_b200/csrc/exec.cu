@@ -653,11 +653,105 @@ static void fuse_pairs(std::vector<Op>& prog, const Ctx& ctx) {
   }
 }
 
+// One local pass of a 3-D block: axis v of the buffer `in` (extents len,
+// element strides si) into `out` (strides so over the output extents).
+static Op single_pass(const Ctx& ctx, int v, int n, const int64_t* len, const int64_t* si,
+                      const void* in, void* out, const int64_t* so, int fkind, double scale) {
+  int lanes[2], nl = 0;
+  for (int a = 0; a < 3; ++a)
+    if (a != v) lanes[nl++] = a;
+  const int ax_a = lanes[0], ax_b = lanes[1];
+  Op op;
+  PassParams& p = op.p;
+  p.in = in;
+  p.A = (int)len[ax_a];
+  p.A1 = 1;
+  p.in_sa1 = 0;
+  p.B = (int)len[ax_b];
+  p.in_sa = si[ax_a];
+  p.in_sb = si[ax_b];
+  p.in_si = si[v];
+  op.n = n;
+  p.n_out = fkind == DFFTB_R2C ? n / 2 + 1 : n;
+  p.in_mode = fkind == DFFTB_R2C ? kInReal : (fkind == DFFTB_C2R ? kInHermitian : kInComplex);
+  p.out_real = fkind == DFFTB_C2R;
+  p.inverse = true;
+  p.scale = scale;
+  p.tw = is_pow2(n) ? ctx.twiddles.at(n) : nullptr;
+  p.herm = ctx.dstat;
+  op.adj = p.in_si != 1;
+  p.ndest = 1;
+  p.oblk = p.n_out > 0 ? p.n_out : 1;
+  Dest& d = p.dest[0];
+  d.ptr = out;
+  d.base = 0;
+  d.sa = so[ax_a];
+  d.sa1 = 0;
+  d.sb = so[ax_b];
+  d.sk = so[v];
+  op.tma = false;
+  set_store_mode(p);
+  op.tma = plan_tma(op, ctx.prec);
+  plan_generic(op, ctx);
+  return op;
+}
+
+// Single-rank 3-D backward: every exchange is local, so the axis order is
+// free (the transforms commute; results agree to rounding).  Run the axes as
+// the forward does — contiguous lanes first, the [x1][x0][rest] buffer feeding
+// the axis-0 pass, strided stores last — instead of the reference's F0;F1;F2
+// order (plan.hpp:293-312), whose first pass would load axis-0 lanes of the
+// user block at a whole-plane stride.  C2R keeps its Hermitian axis last.
+static bool lower_single(const Plan& plan, const Ctx& ctx, const void* d_in, void* d_out, int parity,
+                         std::vector<Op>& prog) {
+  if (plan.nranks() != 1 || plan.input.ndim() != 3 || !zperm_enabled()) return false;
+  {
+    const char* e = getenv("DFFTB_SINGLE_REORDER");
+    if (e && *e == '0') return false;
+  }
+  bool backward = false, c2r = false;
+  double scale = 1.0;
+  for (const auto& st : plan.stages) {
+    if (st.type == StageType::Fft) {
+      backward = st.dir == DFFTB_BACKWARD;
+      if (st.fkind == DFFTB_C2R) c2r = true;
+      if (st.fkind == DFFTB_R2C) return false;
+    } else if (st.type == StageType::Normalize) {
+      scale = st.factor;
+    }
+  }
+  if (!backward) return false;
+  int64_t off[3], lc[3], lr[3];
+  plan.input.extents_of(0, off, lc);    // complex (Hermitian for C2R) extents
+  plan.output.extents_of(0, off, lr);   // output extents
+  for (int a = 0; a < 3; ++a)
+    if (lc[a] <= 0) return false;
+  const int prec = ctx.prec;
+  void* b1 = ctx.exch(0, 0, parity);
+  void* b2 = ctx.exch(0, 1, parity);
+  int64_t s_user[3], s_plain[3], s_swap[3], s_out[3];
+  row_major_strides(lc, 3, s_user, false, prec);
+  row_major_strides(lc, 3, s_plain, true, prec);
+  row_major_strides(lc, 3, s_swap, true, prec, true);
+  row_major_strides(lr, 3, s_out, false, prec);
+  if (!c2r) {
+    prog.push_back(single_pass(ctx, 2, (int)lc[2], lc, s_user, d_in, b1, s_plain, DFFTB_C2C, 1.0));
+    prog.push_back(single_pass(ctx, 1, (int)lc[1], lc, s_plain, b1, b2, s_swap, DFFTB_C2C, 1.0));
+    prog.push_back(single_pass(ctx, 0, (int)lc[0], lc, s_swap, b2, d_out, s_out, DFFTB_C2C, scale));
+  } else {
+    prog.push_back(single_pass(ctx, 1, (int)lc[1], lc, s_user, d_in, b1, s_swap, DFFTB_C2C, 1.0));
+    prog.push_back(single_pass(ctx, 0, (int)lc[0], lc, s_swap, b1, b2, s_plain, DFFTB_C2C, 1.0));
+    prog.push_back(single_pass(ctx, 2, (int)lr[2], lc, s_plain, b2, d_out, s_out, DFFTB_C2R, scale));
+  }
+  return true;
+}
+
 // One rank's program: fused passes and barriers.  `peer` supplies the
 // exchange-buffer base of any world rank (its own mapping of the peers).
 static std::vector<Op> lower(const Plan& plan, const Ctx& ctx, const void* d_in, void* d_out,
                              int parity) {
   std::vector<Op> prog;
+  if (lower_single(plan, ctx, d_in, d_out, parity, prog)) return prog;
   const int me = ctx.rank;
   const void* cur = d_in;
   bool cur_internal = false;  // d_in has the user layout; exch/work are padded

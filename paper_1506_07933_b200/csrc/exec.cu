@@ -254,6 +254,17 @@ Ctx* ctx_create(const Plan& plan, int rank, int device) {
       ctx->fuse_ring_bytes = (size_t)L * plan.dims[1] * plan.dims[2] * 2 * plan.prec;
       CUDA_TRY(cudaMalloc(&ctx->fuse_ring, ctx->fuse_ring_bytes));
       CUDA_TRY(cudaMalloc(&ctx->fuse_counters, 2 * sizeof(unsigned int) * ctx->fuse_planes));
+      // reserve persisting L2 for the ring so its dirty lines are overwritten
+      // in L2 instead of being written back (DFFTB_FUSE_PERSIST=0 disables)
+      const char* pe = getenv("DFFTB_FUSE_PERSIST");
+      if (!(pe && *pe == '0')) {
+        int maxp = 0;
+        cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, device);
+        const size_t want = std::min<size_t>((size_t)maxp, ctx->fuse_ring_bytes);
+        if (want > 0 && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) == cudaSuccess)
+          ctx->fuse_persist_bytes = want;
+        cudaGetLastError();
+      }
     }
   }
   ctx->peer_region.assign(ctx->nranks, nullptr);
@@ -364,6 +375,16 @@ struct Op {
   bool fused = false;
   int grid_axis = 0;
   std::vector<int> members;
+  // lane geometry (for pipelining): transform axis, lane axes, input layout
+  int v = -1, ax_a = -1, ax_b = -1;
+  const Dist* before = nullptr;
+  // pipelined pair: this op's pass (p, tp, adj) is the producer, (pb, tpb,
+  // adj_b) the consumer, on disjoint CTAs of one launch
+  bool pipe = false;
+  bool adj_b = false;
+  TmaPlan tpb{};
+  PipeArgs ppa{}, ppb{};
+  double frac = 0.5;
 };
 
 // Row-major element strides of a block; internal buffers pad the innermost
@@ -622,6 +643,8 @@ static void fuse_pairs(std::vector<Op>& prog, const Ctx& ctx) {
     fa.lag = lag;
     fa.doneA = ctx.fuse_counters;
     fa.doneB = ctx.fuse_counters + ctx.fuse_planes;
+    fa.ring = ctx.fuse_ring;
+    fa.persist_bytes = ctx.fuse_persist_bytes;
     {
       const char* nd = getenv("DFFTB_FUSE_NODEP");
       fa.nodeps = nd && *nd == '1';
@@ -746,9 +769,155 @@ static bool lower_single(const Plan& plan, const Ctx& ctx, const void* d_in, voi
   return true;
 }
 
+// ------------------------------------------------------ pipelined pairs
+//
+// The reference overlaps communication with computation by chunking along
+// the N0/P0 planes (pipelined_all_to_all, exchange.hpp:250-423).
+// Here the two passes on either side of an exchange run concurrently on
+// disjoint CTAs of one launch, chunked along the lane axis both share (the
+// axis the exchange does not touch): while the NVLink-bound pass streams
+// chunk c to the peers, the HBM-bound pass already transforms chunk c - 1.
+// Per-chunk tile counters in every rank's flag page replace the group
+// barrier between the two passes.
+static constexpr int kPipeSlots = 8;
+static constexpr size_t kPipeOffU64 = 256;  // counter slots start after the barrier flags
+
+static bool pipe_candidate(const Op& o, int prec) {
+  if (o.barrier || o.generic || o.fused2 || o.pipe || !o.tma || o.before == nullptr) return false;
+  if (o.tp.args.ldgsts || o.p.A1 > 1 || o.p.A <= 0 || o.p.B <= 0) return false;
+  if (o.p.in_mode != kInComplex || o.p.out_real) return false;
+  return pipe_supported(prec, o.n);
+}
+
+static void pipeline_pairs(std::vector<Op>& prog, Ctx& ctx) {
+  // DFFTB_PIPE_LOCAL=1: also pair two local passes (profiling aid: lets the
+  // pipelined kernel run, and be profiled, on one GPU)
+  const char* pl = getenv("DFFTB_PIPE_LOCAL");
+  const bool local_pairs = pl && *pl == '1';
+  if (ctx.world_mode || (ctx.nranks < 2 && !local_pairs)) return;
+  {
+    // opt-in: measured slower than the sequential passes in round 1
+    const char* e = getenv("DFFTB_PIPE");
+    if (!(e && *e == '1') && !local_pairs) return;
+  }
+  int want = 16;
+  if (const char* e = getenv("DFFTB_PIPE_CHUNKS")) want = std::max(2, std::min(kMaxChunks, atoi(e)));
+  double frac_env = -1.0;
+  if (const char* e = getenv("DFFTB_PIPE_FRAC")) frac_env = atof(e);
+  if ((int)ctx.pipe_cum.size() < kPipeSlots) ctx.pipe_cum.assign(kPipeSlots, {});
+  const int me = ctx.rank;
+  const int prec = ctx.prec;
+  const int64_t csize = 2 * prec;
+  int slot = 0;
+  for (size_t i = 0; i + 1 < prog.size() && slot < kPipeSlots; ++i) {
+    Op& P = prog[i];
+    if (!pipe_candidate(P, prec)) continue;
+    size_t jq = i + 1;
+    const bool bar = prog[jq].barrier;
+    if (bar) ++jq;
+    if (jq >= prog.size()) continue;
+    Op& Q = prog[jq];
+    if (!pipe_candidate(Q, prec) || Q.n != P.n || Q.p.inverse != P.p.inverse) continue;
+    const bool p_remote = P.fused && P.members.size() > 1;
+    const bool q_remote = Q.fused && Q.members.size() > 1;
+    if (p_remote == q_remote && !(local_pairs && !p_remote)) continue;  // only NVLink next to HBM gains
+    // Q reads what P stored for this rank
+    int q_me = 0;
+    if (P.fused)
+      for (size_t q = 0; q < P.members.size(); ++q)
+        if (P.members[q] == me) q_me = (int)q;
+    if (P.p.dest[q_me].ptr != Q.p.in) continue;
+    if (P.before->ndim() != 3 || Q.before->ndim() != 3 || P.v == Q.v) continue;
+    const int X = 3 - P.v - Q.v;
+    if ((X != P.ax_a && X != P.ax_b) || (X != Q.ax_a && X != Q.ax_b)) continue;
+    const bool pbeta = X == P.ax_b, qbeta = X == Q.ax_b;
+    const int W = tma_tile_w(prec, P.n);
+    int64_t offP[kMaxDims], lenP[kMaxDims], offQ[kMaxDims], lenQ[kMaxDims];
+    P.before->extents_of(me, offP, lenP);
+    Q.before->extents_of(me, offQ, lenQ);
+    if (lenP[X] != lenQ[X] || offP[X] != offQ[X]) continue;
+    const int64_t Xe = lenP[X];
+    int64_t R = (Xe + want - 1) / want;
+    if (pbeta || qbeta) R = ((R + W - 1) / W) * W;
+    const int C = (int)((Xe + R - 1) / R);
+    if (C < 2 || C > kMaxChunks) continue;
+    auto tiles_b = [&](int64_t B) { return (B + W - 1) / W; };
+    auto tpc_of = [&](bool beta, int64_t A, int64_t B) { return beta ? (R / W) * A : R * tiles_b(B); };
+    auto in_chunk = [&](bool beta, int64_t A, int64_t B, int c) -> int64_t {
+      if (beta) {
+        const int64_t b0 = c * (R / W), b1 = std::min(b0 + R / W, tiles_b(B));
+        return std::max<int64_t>(0, b1 - b0) * A;
+      }
+      const int64_t a0 = c * R, a1 = std::min(a0 + R, A);
+      return std::max<int64_t>(0, a1 - a0) * tiles_b(B);
+    };
+    // every rank P writes into publishes there; the ranks writing into this
+    // rank's buffer are the same group (symmetric exchange)
+    std::vector<int> writers = p_remote ? P.members : std::vector<int>{me};
+    unsigned long long expect[kMaxChunks] = {};
+    for (int m : writers) {
+      int64_t o[kMaxDims], l[kMaxDims];
+      P.before->extents_of(m, o, l);
+      for (int c = 0; c < C; ++c) expect[c] += (unsigned long long)in_chunk(pbeta, l[P.ax_a], l[P.ax_b], c);
+    }
+    Op M = P;
+    M.pipe = true;
+    M.fused = true;
+    M.pb = Q.p;
+    M.tpb = Q.tp;
+    M.adj_b = Q.adj;
+    PipeArgs& pa = M.ppa;
+    PipeArgs& pq = M.ppb;
+    std::memset(&pa, 0, sizeof(pa));
+    std::memset(&pq, 0, sizeof(pq));
+    pa.order_beta = pbeta ? (int)(R / W) : 0;
+    pa.tpc = tpc_of(pbeta, P.p.A, P.p.B);
+    pa.pub_sys = p_remote;
+    const std::vector<int> targets = p_remote ? P.members : std::vector<int>{me};
+    pa.npub = (int)targets.size();
+    for (size_t q = 0; q < targets.size(); ++q)
+      pa.pub[q] = reinterpret_cast<unsigned long long*>(ctx.flags_of(targets[q])) + kPipeOffU64 +
+                  (size_t)slot * kMaxChunks;
+    pq.order_beta = qbeta ? (int)(R / W) : 0;
+    pq.tpc = tpc_of(qbeta, Q.p.A, Q.p.B);
+    pq.wait = reinterpret_cast<const unsigned long long*>(ctx.flags_of(me)) + kPipeOffU64 +
+              (size_t)slot * kMaxChunks;
+    for (int c = 0; c < C; ++c) {
+      ctx.pipe_cum[slot][c] += expect[c];
+      pq.target[c] = ctx.pipe_cum[slot][c];
+    }
+    pq.timeout_flag = ctx.dstat + 2;
+    pq.timeout_ns = 10ull * 1000 * 1000 * 1000;
+    // CTA split: balance max(SM-bound time, NVLink time) of the two roles
+    if (frac_env > 0.0 && frac_env < 1.0) {
+      M.frac = frac_env;
+    } else {
+      const double sm_rate = 40e9, nvl_rate = 700e9;  // B/s per SM (read + write), per GPU
+      auto role_time = [&](const Op& o, bool remote, double share) {
+        const double rw = 2.0 * (double)o.p.A * o.p.B * o.n * csize;
+        const double nvl = remote ? 0.5 * rw * (double)(o.members.size() - 1) / o.members.size() : 0.0;
+        return std::max(rw / (share * 148.0 * sm_rate), nvl / nvl_rate);
+      };
+      double best = 1e30;
+      for (int g = 8; g <= 140; ++g) {
+        const double f = g / 148.0;
+        const double t = std::max(role_time(P, p_remote, f), role_time(Q, q_remote, 1.0 - f));
+        if (t < best) {
+          best = t;
+          M.frac = f;
+        }
+      }
+    }
+    prog[i] = M;
+    prog.erase(prog.begin() + (long)jq);
+    if (bar) prog.erase(prog.begin() + (long)i + 1);
+    ++slot;
+  }
+}
+
 // One rank's program: fused passes and barriers.  `peer` supplies the
 // exchange-buffer base of any world rank (its own mapping of the peers).
-static std::vector<Op> lower(const Plan& plan, const Ctx& ctx, const void* d_in, void* d_out,
+static std::vector<Op> lower(const Plan& plan, Ctx& ctx, const void* d_in, void* d_out,
                              int parity) {
   std::vector<Op> prog;
   if (lower_single(plan, ctx, d_in, d_out, parity, prog)) return prog;
@@ -783,6 +952,10 @@ static std::vector<Op> lower(const Plan& plan, const Ctx& ctx, const void* d_in,
       if (nl >= 3) ax_a1 = lanes[nl - 3];
     }
     Op op;
+    op.v = v;
+    op.ax_a = ax_a;
+    op.ax_b = ax_b;
+    op.before = &Lb;
     PassParams& p = op.p;
     p.in = cur;
     p.A = ax_a >= 0 ? (int)lenb[ax_a] : 1;
@@ -870,6 +1043,7 @@ static std::vector<Op> lower(const Plan& plan, const Ctx& ctx, const void* d_in,
     }
   }
   fuse_pairs(prog, ctx);
+  pipeline_pairs(prog, ctx);
   return prog;
 }
 
@@ -894,6 +1068,10 @@ static void launch_op(const Ctx& ctx, const Op& op, uint64_t epoch, cudaStream_t
   if (op.fused2) {
     CUDA_TRY(cudaMemsetAsync(op.fa.doneA, 0, 2 * sizeof(unsigned int) * op.fa.P, s));
     CUDA_TRY(launch_fused2(ctx.prec, op.n, op.fwd2, op.p, op.pb, op.tp.tmap, op.fa, s));
+    return;
+  }
+  if (op.pipe) {
+    CUDA_TRY(launch_pipe(ctx.prec, op.n, op.p, op.adj, op.tp, op.ppa, op.pb, op.adj_b, op.tpb, op.ppb, op.frac, s));
     return;
   }
   if (op.generic) CUDA_TRY(launch_generic(ctx.prec, op.g, s));

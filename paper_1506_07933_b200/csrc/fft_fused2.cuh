@@ -36,6 +36,8 @@ struct Fused2Args {
   unsigned int* doneA;  // [P] A tiles stored per plane
   unsigned int* doneB;  // [P] B tiles that pulled their scratch data
   int nodeps;           // timing experiment only: skip dependency waits (wrong results)
+  void* ring;           // host side: the ring, for the L2 access-policy window
+  size_t persist_bytes; // host side: persisting window bytes (0: none)
 };
 
 __device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p) {

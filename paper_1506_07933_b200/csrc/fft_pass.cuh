@@ -42,6 +42,12 @@
 #ifndef DFFTB_TMA_THREADS
 #define DFFTB_TMA_THREADS 512  // threads per CTA of the TMA pass kernel
 #endif
+#ifndef DFFTB_EXP_NOCOMPUTE
+#define DFFTB_EXP_NOCOMPUTE 0  // timing experiment: skip the butterflies (wrong results)
+#endif
+#ifndef DFFTB_EXP_NOSTORE
+#define DFFTB_EXP_NOSTORE 0  // timing experiment: skip the global stores
+#endif
 #ifndef DFFTB_TMA_MINB
 #define DFFTB_TMA_MINB 1    // resident CTAs per SM the TMA kernel is compiled for
 #endif

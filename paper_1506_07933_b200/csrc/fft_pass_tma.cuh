@@ -29,6 +29,26 @@ struct TmaArgs {
   int ldgsts;      // strided lanes: per-thread cp.async (16 B) instead of TMA boxes
 };
 
+// Pipelined pass pairs (SURVEY §8(e) "overlap"): a producer pass and the
+// consumer pass that reads its output run concurrently on disjoint CTAs of
+// one launch.  Tiles are grouped into chunks of `tpc` consecutive tile
+// indices that cover one range of the lane axis both passes share (the axis
+// the exchange does not touch).  The producer adds, per chunk, the number of
+// its tiles stored to a counter on every rank it writes to; the consumer
+// loads a tile of chunk c only once its counter reached target[c].
+constexpr int kMaxChunks = 32;
+struct PipeArgs {
+  int order_beta;  // > 0: chunks span order_beta beta tiles (chunk, alpha, beta order); 0: alpha-major
+  int64_t tpc;     // tiles per chunk (0: not pipelined)
+  int npub;        // producer: ranks written (0: not a producer)
+  int pub_sys;     // producer writes other GPUs: system-scope fence
+  unsigned long long* pub[kMaxDest];
+  const unsigned long long* wait;  // consumer: own counters (nullptr: no waits)
+  unsigned long long target[kMaxChunks];
+  unsigned long long* timeout_flag;
+  unsigned long long timeout_ns;
+};
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -175,34 +195,84 @@ __device__ __forceinline__ void store_lk(const PassParams& p, void* const* sptr,
   }
 }
 
+__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// consumer side: spin until counter >= target (timeout -> flag, carry on)
+__device__ __forceinline__ void pipe_wait(const PipeArgs& pp, int c) {
+  const unsigned long long tgt = pp.target[c];
+  // after one timeout the execute is already failed: do not wait again
+  if (ld_acquire_sys_u64(pp.wait + c) < tgt && ld_acquire_sys_u64(pp.timeout_flag) == 0) {
+    const unsigned long long t0 = globaltimer_ns();
+    while (ld_acquire_sys_u64(pp.wait + c) < tgt) {
+      if (globaltimer_ns() - t0 > pp.timeout_ns) {
+        atomicExch(pp.timeout_flag, 1ull);
+        break;
+      }
+      __nanosleep(128);
+    }
+  }
+  // the chunk was written through the generic proxy; TMA reads it next
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+// The tile loop of one pass over tiles cta, cta + ncta, ...: TMA prefetch of
+// the next STAGES tiles into shared memory while the current tile is
+// transformed and stored.  Shared by the single-pass kernel and both roles of
+// the pipelined pair kernel.
 template <typename T, int N, int EPREF, int W, bool ADJ, int STAGES, int LK>
-__global__ void __launch_bounds__(W* Sched<N, EPREF>::TPL, DFFTB_TMA_MINB)
-    fft_pass_tma_kernel(const __grid_constant__ PassParams p, const __grid_constant__ CUtensorMap tm,
-                        const TmaArgs ta) {
+__device__ __forceinline__ void pass_tiles(const PassParams& p, const CUtensorMap& tm, const TmaArgs& ta,
+                                           const PipeArgs& pp, int cta, int ncta, unsigned char* smem) {
   using C = Cpx<T>;
   using SC = Sched<N, EPREF>;
   using TL = TmaLayout<T, N, W>;
   constexpr int TPL = SC::TPL;
   constexpr int LS = lane_stride<C>(N);
-  extern __shared__ __align__(1024) unsigned char smem_tma[];
-  unsigned char* stg = smem_tma;
-  C* xch = reinterpret_cast<C*>(smem_tma + STAGES * TL::STG);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_tma + STAGES * TL::STG + TL::XCH);
+  unsigned char* stg = smem;
+  C* xch = reinterpret_cast<C*>(smem + STAGES * TL::STG);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * TL::STG + TL::XCH);
   void** sptr = reinterpret_cast<void**>(bars + STAGES);  // destination pointers
 
   const int tid = threadIdx.x;
   const int w = ADJ ? tid % W : tid / TPL;
   const int j = ADJ ? tid / W : tid % TPL;
   const int tiles_b = (p.B + W - 1) / W;
-  C* lane = xch + w * LS;
   const C* tw = reinterpret_cast<const C*>(p.tw);
   constexpr int ESIZE = LK == kR2C ? (int)sizeof(T) : (int)sizeof(C);
   const T sc = static_cast<T>(p.scale);
 
+  auto decode = [&](int64_t t, int& alpha, int& beta0) {
+    int64_t bc;
+    if (pp.order_beta) {
+      // chunk-major, then alpha, then the chunk's beta tiles: concurrent CTAs
+      // still cover adjacent lanes (contiguous rows) inside a chunk
+      const int64_t bpc = pp.order_beta;  // beta tiles per chunk
+      const int64_t c = t / pp.tpc;
+      const int64_t r = t - c * pp.tpc;
+      const int64_t width = min(bpc, (int64_t)tiles_b - c * bpc);
+      const int64_t a = r / width;
+      alpha = (int)a;
+      bc = c * bpc + (r - a * width);
+    } else {
+      alpha = (int)(t / tiles_b);
+      bc = t - (int64_t)alpha * tiles_b;
+    }
+    beta0 = (int)bc * W;
+  };
+
   // called by every thread; TMA ops are issued by thread 0 only
   auto issue = [&](int64_t t, int s) {
-    const int alpha = (int)(t / tiles_b);
-    const int beta0 = (int)(t - (int64_t)alpha * tiles_b) * W;
+    int alpha, beta0;
+    decode(t, alpha, beta0);
     unsigned char* dst = stg + s * TL::STG;
     if (ADJ && ta.ldgsts) {
       // very large row strides (e.g. the axis-0 pass) translate one page per
@@ -222,6 +292,7 @@ __global__ void __launch_bounds__(W* Sched<N, EPREF>::TPL, DFFTB_TMA_MINB)
       return;
     }
     if (tid != 0) return;
+    if (pp.wait) pipe_wait(pp, (int)(t / pp.tpc));
     if constexpr (ADJ) {
       mbar_expect_tx(&bars[s], (uint32_t)(W * N * sizeof(C)));
       for (int r0 = 0; r0 < N; r0 += ta.rows) {
@@ -246,17 +317,19 @@ __global__ void __launch_bounds__(W* Sched<N, EPREF>::TPL, DFFTB_TMA_MINB)
   if (tid < kMaxDest) sptr[tid] = p.dest[tid].ptr;
   __syncthreads();
   for (int s = 0; s < STAGES; ++s) {
-    const int64_t t = blockIdx.x + (int64_t)s * gridDim.x;
+    const int64_t t = cta + (int64_t)s * ncta;
     if (t < ta.ntiles) issue(t, s);
   }
 
   T lmax = T(0), limag = T(0);  // C2R statistics, reduced once per CTA at the end
+  unsigned long long done = 0;  // producer: tiles stored in the current chunk
   int k = 0;
-  for (int64_t t = blockIdx.x; t < ta.ntiles; t += gridDim.x, ++k) {
+  for (int64_t t = cta; t < ta.ntiles; t += ncta, ++k) {
     const int s = k % STAGES;
     mbar_wait(&bars[s], (uint32_t)((k / STAGES) & 1));
-    const int alpha = (int)(t / tiles_b);
-    const int beta = (int)(t - (int64_t)alpha * tiles_b) * W + w;
+    int alpha, beta;
+    decode(t, alpha, beta);
+    beta += w;
     const unsigned char* st = stg + s * TL::STG;
     C v[SC::E];
     if constexpr (ADJ) {
@@ -286,16 +359,69 @@ __global__ void __launch_bounds__(W* Sched<N, EPREF>::TPL, DFFTB_TMA_MINB)
     }
     __syncthreads();  // staging slot s fully consumed by every thread
     {
-      const int64_t t2 = t + (int64_t)STAGES * gridDim.x;
+      const int64_t t2 = t + (int64_t)STAGES * ncta;
       if (t2 < ta.ntiles) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         issue(t2, s);
       }
     }
-    run_stages<T, N, EPREF, 0>(v, lane, tw, j);
+#if DFFTB_EXP_NOCOMPUTE  // timing experiment only (wrong results): data movement alone
+    (void)tw;
+#else
+    run_stages<T, N, EPREF, 0>(v, xch + w * LS, tw, j);
+#endif
+#if DFFTB_EXP_NOSTORE  // timing experiment only: compute without the global stores
+    if (p.scale == 12345.0 && beta < p.B) store_lk<T, N, EPREF, LK>(p, sptr, v, j, alpha, beta, sc);
+#else
     if (beta < p.B) store_lk<T, N, EPREF, LK>(p, sptr, v, j, alpha, beta, sc);
+#endif
+    if (pp.npub) {
+      // producer: publish a chunk once this CTA has no further tile in it
+      ++done;
+      const int64_t c = t / pp.tpc;
+      if (t + ncta >= ta.ntiles || (t + ncta) / pp.tpc != c) {
+        if (pp.pub_sys) __threadfence_system();
+        else __threadfence();
+        __syncthreads();
+        if (tid == 0) {
+          for (int q = 0; q < pp.npub; ++q) {
+            if (pp.pub_sys)
+              asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(pp.pub[q] + c), "l"(done) : "memory");
+            else
+              asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(pp.pub[q] + c), "l"(done) : "memory");
+          }
+        }
+        done = 0;
+      }
+    }
   }
   if constexpr (LK == kC2R) herm_reduce<T>(p.herm, lmax, limag);
+}
+
+template <typename T, int N, int EPREF, int W, bool ADJ, int STAGES, int LK>
+__global__ void __launch_bounds__(W* Sched<N, EPREF>::TPL, DFFTB_TMA_MINB)
+    fft_pass_tma_kernel(const __grid_constant__ PassParams p, const __grid_constant__ CUtensorMap tm,
+                        const TmaArgs ta) {
+  extern __shared__ __align__(1024) unsigned char smem_tma[];
+  const PipeArgs pp{};  // single pass: natural tile order, no chunk protocol
+  pass_tiles<T, N, EPREF, W, ADJ, STAGES, LK>(p, tm, ta, pp, blockIdx.x, gridDim.x, smem_tma);
+}
+
+// Pipelined pair: CTAs [0, ncta_a) run the producer pass, the rest the
+// consumer.  One launch, so both roles are co-resident (grid <= SMs x
+// occupancy): the consumer's waits can always be satisfied.
+template <typename T, int N, int EPREF, int W, bool ADJ_A, bool ADJ_B, int STAGES, int LK>
+__global__ void __launch_bounds__(W* Sched<N, EPREF>::TPL, DFFTB_TMA_MINB)
+    fft_pipe_kernel(const __grid_constant__ PassParams pa, const __grid_constant__ CUtensorMap tma,
+                    const __grid_constant__ TmaArgs taa, const __grid_constant__ PipeArgs ppa,
+                    const __grid_constant__ PassParams pb, const __grid_constant__ CUtensorMap tmb,
+                    const __grid_constant__ TmaArgs tab, const __grid_constant__ PipeArgs ppb, int ncta_a) {
+  extern __shared__ __align__(1024) unsigned char smem_tma[];
+  if ((int)blockIdx.x < ncta_a)
+    pass_tiles<T, N, EPREF, W, ADJ_A, STAGES, LK>(pa, tma, taa, ppa, blockIdx.x, ncta_a, smem_tma);
+  else
+    pass_tiles<T, N, EPREF, W, ADJ_B, STAGES, LK>(pb, tmb, tab, ppb, blockIdx.x - ncta_a,
+                                                   gridDim.x - ncta_a, smem_tma);
 }
 
 }  // namespace dfftb

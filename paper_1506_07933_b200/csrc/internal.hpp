@@ -6,6 +6,7 @@
 // group barriers for one rank.
 #pragma once
 
+#include <array>
 #include <cstdint>
 #include <map>
 #include <memory>
@@ -127,6 +128,7 @@ struct Ctx {
   unsigned long long* dstat = nullptr;  // [0] herm max, [1] herm imag, [2] timeout flag, [3] nonfinite
   void* fuse_ring = nullptr;            // L2-resident plane ring of the fused two-axis pass
   size_t fuse_ring_bytes = 0;
+  size_t fuse_persist_bytes = 0;        // persisting-L2 carve-out reserved for the ring
   unsigned int* fuse_counters = nullptr;  // [2 * fuse_planes]
   int fuse_planes = 0;
   std::map<int, void*> twiddles;        // N -> device table (prec of the ctx)
@@ -138,6 +140,9 @@ struct Ctx {
   bool world_mode = false;
   uint64_t epoch = 0;
   uint64_t exec_count = 0;
+  // pipelined pass pairs: cumulative per-chunk counter targets of each
+  // counter slot (identical on every rank: all ranks run the same programs)
+  std::vector<std::array<unsigned long long, 32>> pipe_cum;
   bool c2r_pending = false;
 
   void* exch(int rank, int slot, int parity) const;

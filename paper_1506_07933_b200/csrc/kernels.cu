@@ -169,6 +169,7 @@ static int tma_w_prec(int n) {
 
 int tma_tile_w(int prec, int n) { return prec == 8 ? tma_w_prec<double>(n) : tma_w_prec<float>(n); }
 
+
 // ----------------------------------------------- fused two-axis plane pipeline
 
 template <typename T, int N, bool FWD>
@@ -193,9 +194,26 @@ static cudaError_t launch_fused2_tn(const PassParams& pa, const PassParams& pb, 
   }
   const int64_t items = (int64_t)(fa.P + fa.lag) * 2 * fa.T;
   const int64_t grid = items < grid_cap[dev] ? items : grid_cap[dev];
-  kern<<<(unsigned)grid, Cf::THREADS, SMEM, s>>>(pa, pb, tm, fa);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(Cf::THREADS);
+  cfg.dynamicSmemBytes = SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  if (fa.persist_bytes > 0) {
+    // the ring persists in L2; everything else streams through
+    attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
+    attr[0].val.accessPolicyWindow.base_ptr = fa.ring;
+    attr[0].val.accessPolicyWindow.num_bytes = fa.persist_bytes;
+    attr[0].val.accessPolicyWindow.hitRatio = 1.0f;
+    attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  }
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, pa, pb, tm, fa);
   count_launch();
-  return cudaGetLastError();
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 template <typename T>
@@ -218,6 +236,70 @@ cudaError_t launch_fused2(int prec, int n, bool fwd, const PassParams& pa, const
                           const CUtensorMap& tm, const Fused2Args& fa, cudaStream_t s) {
   return prec == 8 ? launch_fused2_prec<double>(n, fwd, pa, pb, tm, fa, s)
                    : launch_fused2_prec<float>(n, fwd, pa, pb, tm, fa, s);
+}
+
+// ------------------------------------------------ pipelined pass pairs
+
+template <typename T, int N, bool ADJ_A, bool ADJ_B, int LK>
+static cudaError_t launch_pipe_tn(const PassParams& pa, const TmaPlan& ta, const PipeArgs& ppa,
+                                  const PassParams& pb, const TmaPlan& tb, const PipeArgs& ppb, double frac_a,
+                                  cudaStream_t s) {
+  using Cf = TmaCfg<T, N>;
+  auto kern = fft_pipe_kernel<T, N, Cf::EPREF, Cf::W, ADJ_A, ADJ_B, Cf::STAGES, LK>;
+  static int grid_cap[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  if (!grid_cap[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM);
+    if (e != cudaSuccess) return e;
+    int occ = 0, sms = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Cf::THREADS, Cf::SMEM);
+    if (e != cudaSuccess) return e;
+    if (occ < 1) return cudaErrorInvalidConfiguration;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    grid_cap[dev] = occ * sms;  // every CTA co-resident: the consumer's waits always resolve
+  }
+  const int cap = grid_cap[dev];
+  int na = (int)(frac_a * cap + 0.5);
+  na = na < 1 ? 1 : (na > cap - 1 ? cap - 1 : na);
+  kern<<<(unsigned)cap, Cf::THREADS, Cf::SMEM, s>>>(pa, ta.tmap, ta.args, ppa, pb, tb.tmap, tb.args, ppb, na);
+  count_launch();
+  return cudaGetLastError();
+}
+
+template <typename T, int N>
+static cudaError_t launch_pipe_n(const PassParams& pa, bool adj_a, const TmaPlan& ta, const PipeArgs& ppa,
+                                 const PassParams& pb, bool adj_b, const TmaPlan& tb, const PipeArgs& ppb,
+                                 double frac_a, cudaStream_t s) {
+  const bool bwd = pa.inverse != 0;
+#define DFFTB_PIPE(AA, AB)                                                                            \
+  if (adj_a == AA && adj_b == AB)                                                                     \
+    return bwd ? launch_pipe_tn<T, N, AA, AB, kC2CBwd>(pa, ta, ppa, pb, tb, ppb, frac_a, s)           \
+               : launch_pipe_tn<T, N, AA, AB, kC2CFwd>(pa, ta, ppa, pb, tb, ppb, frac_a, s);
+  DFFTB_PIPE(false, true)
+  DFFTB_PIPE(true, true)
+  DFFTB_PIPE(true, false)
+#undef DFFTB_PIPE
+  return cudaErrorInvalidValue;
+}
+
+bool pipe_supported(int prec, int n) { return (prec == 8 || prec == 4) && (n == 256 || n == 512 || n == 1024); }
+
+cudaError_t launch_pipe(int prec, int n, const PassParams& pa, bool adj_a, const TmaPlan& ta, const PipeArgs& ppa,
+                        const PassParams& pb, bool adj_b, const TmaPlan& tb, const PipeArgs& ppb, double frac_a,
+                        cudaStream_t s) {
+#define DFFTB_PIPE_N(NN)                                                                              \
+  case NN:                                                                                            \
+    return prec == 8 ? launch_pipe_n<double, NN>(pa, adj_a, ta, ppa, pb, adj_b, tb, ppb, frac_a, s)   \
+                     : launch_pipe_n<float, NN>(pa, adj_a, ta, ppa, pb, adj_b, tb, ppb, frac_a, s);
+  switch (n) {
+    DFFTB_PIPE_N(256)
+    DFFTB_PIPE_N(512)
+    DFFTB_PIPE_N(1024)
+  }
+#undef DFFTB_PIPE_N
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_pass_tma(int prec, int n, const PassParams& p, bool adj, const TmaPlan& tp,

@@ -42,6 +42,10 @@ int tma_tile_w(int prec, int n);  // lanes per CTA of the TMA kernel
 bool fused2_supported(int prec, int n);
 cudaError_t launch_fused2(int prec, int n, bool fwd, const PassParams& pa, const PassParams& pb,
                           const CUtensorMap& tm, const Fused2Args& fa, cudaStream_t s);
+bool pipe_supported(int prec, int n);
+cudaError_t launch_pipe(int prec, int n, const PassParams& pa, bool adj_a, const TmaPlan& ta, const PipeArgs& ppa,
+                        const PassParams& pb, bool adj_b, const TmaPlan& tb, const PipeArgs& ppb, double frac_a,
+                        cudaStream_t s);
 cudaError_t launch_pass_tma(int prec, int n, const PassParams& p, bool adj, const TmaPlan& tp,
                             cudaStream_t s);
 cudaError_t launch_pass(int prec, int n, const PassParams& p, bool adj, cudaStream_t s);

@@ -206,6 +206,16 @@ enum { DFFTB_SPECTRAL_DERIV = 0, DFFTB_SPECTRAL_LAPLACIAN = 1, DFFTB_SPECTRAL_IN
 dfftb_status dfftb_spectral_apply(dfftb_plan forward_plan, int rank, int op, int axis,
                                   const double* domain_lengths, const void* d_in, void* d_out,
                                   int accumulate, void* stream);
+/* Forward transform of d_in with a spectral operator fused into the last
+ * pass's store epilogue: d_out (+)= op(execute(forward_plan, d_in)), the same
+ * values as dfftb_execute followed by dfftb_spectral_apply, with one pass
+ * over the spectrum less.  Collective like dfftb_execute (replaces the
+ * forward-then-multiply pair in derivative / laplacian / inverse_laplacian /
+ * divergence, spectral.hpp:131-309).  The k = 0 owner checks the zero mean
+ * for DFFTB_SPECTRAL_INV_LAPLACIAN (NonZeroMean). */
+dfftb_status dfftb_execute_spectral(dfftb_plan forward_plan, dfftb_ctx ctx, const void* d_in, void* d_out,
+                                    int op, int axis, const double* domain_lengths, int accumulate,
+                                    void* stream, int flags);
 /* wavenumbers (spectral.hpp:24-56): the local k values of `axis` for this
  * rank's frequency block (length = local extent); deriv != 0 gives
  * axis_k_deriv (Nyquist zeroed), else axis_k. */

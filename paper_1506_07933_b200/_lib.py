@@ -64,6 +64,8 @@ _SIGS = {
     "dfftb_kernel_launch_count": (_c.c_uint64, []),
     "dfftb_spectral_apply": (_c.c_int, [vp, _c.c_int, _c.c_int, _c.c_int,
                                         _c.POINTER(_c.c_double), vp, vp, _c.c_int, vp]),
+    "dfftb_execute_spectral": (_c.c_int, [vp, vp, vp, vp, _c.c_int, _c.c_int, _c.POINTER(_c.c_double),
+                                          _c.c_int, vp, _c.c_int]),
     "dfftb_wavenumbers": (_c.c_int, [vp, _c.c_int, _c.c_int, _c.c_int,
                                      _c.POINTER(_c.c_double), _c.POINTER(_c.c_double)]),
 }
@@ -82,6 +84,8 @@ def lib():
                 "`make -C paper_1506_07933_b200/csrc`")
         L = _c.CDLL(LIB_PATH)
         for name, (res, args) in _SIGS.items():
+            if os.environ.get("DFFTB_LIB_OVERRIDE") and not hasattr(L, name):
+                continue  # A/B builds of older revisions may lack newer entry points
             fn = getattr(L, name)
             fn.restype = res
             fn.argtypes = args

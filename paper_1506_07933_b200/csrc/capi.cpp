@@ -274,6 +274,15 @@ dfftb_status dfftb_spectral_apply(dfftb_plan forward_plan, int rank, int op, int
   });
 }
 
+dfftb_status dfftb_execute_spectral(dfftb_plan forward_plan, dfftb_ctx ctx, const void* d_in, void* d_out,
+                                    int op, int axis, const double* domain_lengths, int accumulate,
+                                    void* stream, int flags) {
+  return guarded([&] {
+    dfftb::execute_spectral(forward_plan->plan, *ctx->ctx, d_in, d_out, op, axis, domain_lengths, accumulate,
+                            static_cast<cudaStream_t>(stream), flags);
+  });
+}
+
 dfftb_status dfftb_wavenumbers(dfftb_plan forward_plan, int rank, int axis, int deriv,
                                const double* domain_lengths, double* k_out) {
   return guarded(

@@ -376,7 +376,7 @@ struct Op {
   int grid_axis = 0;
   std::vector<int> members;
   // lane geometry (for pipelining): transform axis, lane axes, input layout
-  int v = -1, ax_a = -1, ax_b = -1;
+  int v = -1, ax_a = -1, ax_b = -1, ax_a1 = -1;
   const Dist* before = nullptr;
   // pipelined pair: this op's pass (p, tp, adj) is the producer, (pb, tpb,
   // adj_b) the consumer, on disjoint CTAs of one launch
@@ -955,6 +955,7 @@ static std::vector<Op> lower(const Plan& plan, Ctx& ctx, const void* d_in, void*
     op.v = v;
     op.ax_a = ax_a;
     op.ax_b = ax_b;
+    op.ax_a1 = ax_a1;
     op.before = &Lb;
     PassParams& p = op.p;
     p.in = cur;
@@ -1135,6 +1136,9 @@ struct EventTimer {
   }
 };
 
+static void run_program(const Plan& plan, Ctx& ctx, const std::vector<Op>& prog, cudaStream_t s, int flags,
+                        dfftb_timing* timers);
+
 void execute(const Plan& plan, Ctx& ctx, const void* d_in, void* d_out, cudaStream_t s, int flags,
              dfftb_timing* timers) {
   DeviceGuard g(ctx.device);
@@ -1143,6 +1147,11 @@ void execute(const Plan& plan, Ctx& ctx, const void* d_in, void* d_out, cudaStre
   const int parity = (int)(ctx.exec_count & 1);
   ctx.exec_count++;
   auto prog = lower(plan, ctx, d_in, d_out, parity);
+  run_program(plan, ctx, prog, s, flags, timers);
+}
+
+static void run_program(const Plan& plan, Ctx& ctx, const std::vector<Op>& prog, cudaStream_t s, int flags,
+                        dfftb_timing* timers) {
   if (plan_has_c2r(plan)) {
     CUDA_TRY(cudaMemsetAsync(ctx.dstat, 0, 2 * sizeof(unsigned long long), s));
     ctx.c2r_pending = true;
@@ -1273,6 +1282,92 @@ void spectral_apply(const Plan& plan, int rank, int op, int axis, const double* 
     }
   }
   CUDA_TRY(launch_spectral(plan.prec, sp, in, out, s));
+}
+
+// Forward transform with the spectral multiplier fused into the last pass's
+// store epilogue: one read + one write of the spectrum
+// less than execute + spectral_apply, bit-identical results.  Lengths the
+// generic (non-power-of-two) kernel handles take the two-step path.
+void execute_spectral(const Plan& plan, Ctx& ctx, const void* d_in, void* d_out, int op, int axis,
+                      const double* lengths, int accumulate, cudaStream_t s, int flags) {
+  DeviceGuard dg(ctx.device);
+  check_compatible(plan, ctx);
+  if (ctx.world_mode) raise(DFFTB_ConfigInvalid, "execute_spectral needs a per-rank context (not an emulated world)");
+  const SpectralParams sp = spectral_params(plan, ctx.rank, lengths);
+  if (op < 0 || op > 2) raise(DFFTB_ConfigInvalid, "unknown spectral operator");
+  if (op == 0 && (axis < 0 || axis >= sp.nd)) raise(DFFTB_OutOfRange, "derivative axis out of range");
+  if (plan.options.validate_finite) validate_finite(plan, ctx, d_in, s);
+  const int parity = (int)(ctx.exec_count & 1);
+  ctx.exec_count++;
+  auto prog = lower(plan, ctx, d_in, d_out, parity);
+  Op* last = prog.empty() ? nullptr : &prog.back();
+  const bool fusable = last && !last->barrier && !last->generic && !last->fused2 && !last->pipe &&
+                       last->before && last->p.ndest == 1 && last->p.dest[0].ptr == d_out &&
+                       !last->p.inverse && last->p.in_mode == kInComplex && !last->p.out_real;
+  const char* nf = getenv("DFFTB_SPECTRAL_UNFUSED");
+  if (!fusable || (nf && *nf == '1')) {
+    run_program(plan, ctx, prog, s, 0, nullptr);
+    spectral_apply(plan, ctx.rank, op, axis, lengths, d_out, d_out, accumulate, s);
+    if (flags & DFFTB_EXEC_SYNC) ctx_check(ctx, s);
+    return;
+  }
+  SpecEpi& e = last->p.spec;
+  std::memset(&e, 0, sizeof(e));
+  e.op = op + 1;
+  e.accumulate = accumulate;
+  const int roles[4] = {last->v, last->ax_a, last->ax_b, last->ax_a1};
+  int64_t off[kMaxDims], len[kMaxDims];
+  last->before->extents_of(ctx.rank, off, len);
+  e.nroles = 0;
+  bool owns_dc = true;
+  for (int r = 0; r < 4; ++r) {
+    const int a = roles[r];
+    if (a < 0) {
+      // absent lane axis (2-D): a zero coordinate of a length-1 axis
+      e.off[r] = 0;
+      e.n[r] = 1;
+      e.half[r] = 0;
+      e.scale[r] = 0.0;
+      continue;
+    }
+    e.nroles = r + 1;
+    e.off[r] = r == 0 ? 0 : off[a];
+    e.n[r] = sp.n[a];
+    e.half[r] = sp.half[a];
+    e.scale[r] = sp.scale[a];
+    if (op == 0 && a == axis) e.deriv_role = r;
+    if (r > 0 && off[a] != 0) owns_dc = false;
+  }
+  // |k|^2 summed in tensor-axis order (as spectral_kernel): bit-identical
+  {
+    int n = 0;
+    for (int a = 0; a < sp.nd; ++a)
+      for (int r = 0; r < 4; ++r)
+        if (roles[r] == a) e.order[n++] = r;
+    e.nroles = n;
+  }
+  if (last->tma) {
+    // the multiplier variant exists for the strided-lane kernel only
+    if (!last->adj) last->tma = false;
+  }
+  const bool check_mean = op == 2 && owns_dc && sp.count > 0;
+  if (check_mean) {
+    CUDA_TRY(cudaMemsetAsync(ctx.dstat + 4, 0, 2 * sizeof(unsigned long long), s));
+    e.dc = ctx.dstat + 4;
+  }
+  run_program(plan, ctx, prog, s, 0, nullptr);
+  if (check_mean) {
+    unsigned long long bits[2];
+    CUDA_TRY(cudaMemcpyAsync(bits, ctx.dstat + 4, sizeof(bits), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    double v[2];
+    std::memcpy(v, bits, sizeof(v));
+    double total = 1;
+    for (auto d : plan.dims) total *= (double)d;
+    if (std::hypot(v[0], v[1]) > 1e-12 * total)
+      raise(DFFTB_NonZeroMean, "inverse_laplacian needs a zero-mean field");
+  }
+  if (flags & DFFTB_EXEC_SYNC) ctx_check(ctx, s);
 }
 
 void wavenumbers(const Plan& plan, int rank, int axis, int deriv, const double* lengths, double* k_out) {

@@ -19,6 +19,8 @@ void execute_world(const Plan& plan, Ctx** ctxs, const void* const* d_in, void* 
                    cudaStream_t s, int flags);
 void spectral_apply(const Plan& plan, int rank, int op, int axis, const double* lengths, const void* in,
                     void* out, int accumulate, cudaStream_t s);
+void execute_spectral(const Plan& plan, Ctx& ctx, const void* d_in, void* d_out, int op, int axis,
+                      const double* lengths, int accumulate, cudaStream_t s, int flags);
 void wavenumbers(const Plan& plan, int rank, int axis, int deriv, const double* lengths, double* k_out);
 void fill_seeded(const Plan& plan, int rank, int side, uint64_t seed, int complex_field, void* d_buf,
                  cudaStream_t s);

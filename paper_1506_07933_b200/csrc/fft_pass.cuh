@@ -78,6 +78,24 @@ struct Dest {
 
 enum InMode : int { kInComplex = 0, kInReal = 1, kInHermitian = 2 };
 
+// Spectral multiplier applied in the store epilogue of the last forward pass
+// (the i k / -|k|^2 factors of spectral.hpp:133-309
+// fused into the FFT instead of a separate pass over the spectrum).  Roles:
+// 0 the transformed axis (index k), 1 the alpha lane axis, 2 beta, 3 the 4-D
+// outer lane axis.
+struct SpecEpi {
+  int op;          // 0 none, 1 derivative, 2 laplacian, 3 inverse laplacian
+  int accumulate;  // out += multiplier * x (divergence)
+  int deriv_role;  // derivative: the role carrying the derivative axis
+  int nroles;
+  int64_t off[4];  // global offset of each role's local index (role 0: 0)
+  int64_t n[4];    // spatial length of each role's axis
+  int half[4];     // role stored as a half spectrum (R2C axis)
+  double scale[4]; // 2 pi / L
+  int order[4];    // roles in tensor-axis order (|k|^2 summed as spectral_kernel does)
+  unsigned long long* dc;  // [2]: raw DC bin (zero-mean check), doubles as bits
+};
+
 struct PassParams {
   const void* in;
   int64_t in_sa, in_sb, in_si;  // strides in elements of the input type
@@ -95,8 +113,70 @@ struct PassParams {
   double scale;
   const void* tw;               // N complex twiddles exp(-2 pi i m / N)
   unsigned long long* herm;     // C2R: [0] max |X| bits, [1] max |Im DC/Nyq| bits
+  SpecEpi spec;                 // spectral epilogue (spec.op == 0: none)
   Dest dest[kMaxDest];
 };
+
+// signed wavenumber (spectral.hpp:42-53), as wavenumber() in kernels.cu
+__device__ __forceinline__ double spec_k(const SpecEpi& e, int role, int64_t g, bool deriv) {
+  int64_t k = g;
+  if (!e.half[role] && 2 * g >= e.n[role]) k = g - e.n[role];
+  const bool nyq = e.n[role] % 2 == 0 && 2 * (k < 0 ? -k : k) == e.n[role];
+  return (deriv && nyq) ? 0.0 : e.scale[role] * (double)k;
+}
+
+// Store of one finished output element with the spectral multiplier
+// (double arithmetic on the T-rounded FFT value, as the separate
+// spectral_kernel: fused and unfused results are bit-identical).
+template <typename T>
+__device__ __forceinline__ void spec_store(const PassParams& p, void* base, int64_t off, Cpx<T> x, int k,
+                                           int alpha, int beta) {
+  const SpecEpi& e = p.spec;
+  int64_t g[4];
+  g[0] = k;
+  int a2 = alpha, a1 = 0;
+  if (p.A1 > 1) {
+    a1 = alpha / p.A;
+    a2 = alpha - a1 * p.A;
+  }
+  g[1] = e.off[1] + a2;
+  g[2] = e.off[2] + beta;
+  g[3] = e.off[3] + a1;
+  if (e.dc && g[0] == 0 && g[1] == 0 && g[2] == 0 && (e.nroles < 4 || g[3] == 0)) {
+    e.dc[0] = static_cast<unsigned long long>(__double_as_longlong((double)x.x));
+    e.dc[1] = static_cast<unsigned long long>(__double_as_longlong((double)x.y));
+  }
+  double re, im;
+  if (e.op == 1) {
+    const double kk = spec_k(e, e.deriv_role, g[e.deriv_role], true);
+    re = -kk * (double)x.y;
+    im = kk * (double)x.x;
+  } else {
+    double m = 0.0;
+    for (int i = 0; i < e.nroles; ++i) {
+      const int r = e.order[i];
+      const double kk = spec_k(e, r, g[r], false);
+      m += kk * kk;
+    }
+    if (e.op == 2) {
+      re = -m * (double)x.x;
+      im = -m * (double)x.y;
+    } else if (m == 0.0) {
+      re = im = 0.0;
+    } else {
+      re = (double)x.x / -m;
+      im = (double)x.y / -m;
+    }
+  }
+  Cpx<T> r{(T)re, (T)im};
+  Cpx<T>* out = reinterpret_cast<Cpx<T>*>(base) + off;
+  if (e.accumulate) {
+    const Cpx<T> o = *out;
+    r.x += o.x;
+    r.y += o.y;
+  }
+  *out = r;
+}
 
 // combined outer lane index alpha = a1 * A + a2 (a1 only for 4-D tensors)
 __device__ __forceinline__ int64_t in_alpha_off(const PassParams& p, int alpha) {
@@ -375,7 +455,11 @@ __device__ __forceinline__ void store_out(const PassParams& p, const Cpx<T>* v, 
       const int64_t off = d.base + dst_alpha_off(p, d, alpha) + (int64_t)beta * d.sb + (int64_t)kk * d.sk;
       C x = v[t * RL + r];
       if (p.inverse) x.y = -x.y;
-      if (p.out_real) {
+      if (p.spec.op) {
+        x.x *= sc;
+        x.y *= sc;
+        spec_store<T>(p, d.ptr, off, x, k, alpha, beta);
+      } else if (p.out_real) {
         reinterpret_cast<T*>(d.ptr)[off] = x.x * sc;
       } else {
         x.x *= sc;

@@ -136,7 +136,7 @@ __device__ __forceinline__ void fetch0_lk(Cpx<T>* v, int j, LDC ldc, LDR ldr) {
 }
 
 // final store, compile-time lane kind; per-tile addressing precomputed
-template <typename T, int N, int EPREF, int LK>
+template <typename T, int N, int EPREF, int LK, bool SPEC = false>
 __device__ __forceinline__ void store_lk(const PassParams& p, void* const* sptr, const Cpx<T>* v,
                                          int j, int alpha, int beta, T sc) {
   using C = Cpx<T>;
@@ -147,8 +147,14 @@ __device__ __forceinline__ void store_lk(const PassParams& p, void* const* sptr,
   constexpr int RL = S > 0 ? SC::radix(S - 1) : 1;
   constexpr int NSL = S > 0 ? SC::ns(S - 1) : 1;
   constexpr int NBL = E / RL;
-  auto put = [&](void* base, int64_t off, C x) {
+  auto put = [&](void* base, int64_t off, C x, int k) {
     if constexpr (LK == kC2CBwd) x.y = -x.y;
+    if constexpr (SPEC && LK != kC2R) {
+      x.x *= sc;
+      x.y *= sc;
+      spec_store<T>(p, base, off, x, k, alpha, beta);
+      return;
+    }
     if constexpr (LK == kC2R) {
       reinterpret_cast<T*>(base)[off] = x.x * sc;
     } else {
@@ -170,11 +176,11 @@ __device__ __forceinline__ void store_lk(const PassParams& p, void* const* sptr,
           if (k > N / 2) continue;
         }
         if (p.store_mode == 0) {
-          put(d0.ptr, tile + (int64_t)k * sk, v[t * RL + r]);
+          put(d0.ptr, tile + (int64_t)k * sk, v[t * RL + r], k);
         } else {
           const int q = k >> p.oshift;
           const int kk = k & p.omask;
-          put(sptr[q], tile + (int64_t)kk * sk, v[t * RL + r]);
+          put(sptr[q], tile + (int64_t)kk * sk, v[t * RL + r], k);
         }
       }
     }
@@ -189,7 +195,7 @@ __device__ __forceinline__ void store_lk(const PassParams& p, void* const* sptr,
         const int kk = k - static_cast<int>(q * p.oblk);
         const Dest& d = p.dest[q];
         put(d.ptr, d.base + dst_alpha_off(p, d, alpha) + (int64_t)beta * d.sb + (int64_t)kk * d.sk,
-            v[t * RL + r]);
+            v[t * RL + r], k);
       }
     }
   }
@@ -229,7 +235,7 @@ __device__ __forceinline__ void pipe_wait(const PipeArgs& pp, int c) {
 // the next STAGES tiles into shared memory while the current tile is
 // transformed and stored.  Shared by the single-pass kernel and both roles of
 // the pipelined pair kernel.
-template <typename T, int N, int EPREF, int W, bool ADJ, int STAGES, int LK>
+template <typename T, int N, int EPREF, int W, bool ADJ, int STAGES, int LK, bool SPEC = false, bool PIPE = false>
 __device__ __forceinline__ void pass_tiles(const PassParams& p, const CUtensorMap& tm, const TmaArgs& ta,
                                            const PipeArgs& pp, int cta, int ncta, unsigned char* smem) {
   using C = Cpx<T>;
@@ -252,7 +258,7 @@ __device__ __forceinline__ void pass_tiles(const PassParams& p, const CUtensorMa
 
   auto decode = [&](int64_t t, int& alpha, int& beta0) {
     int64_t bc;
-    if (pp.order_beta) {
+    if (PIPE && pp.order_beta) {
       // chunk-major, then alpha, then the chunk's beta tiles: concurrent CTAs
       // still cover adjacent lanes (contiguous rows) inside a chunk
       const int64_t bpc = pp.order_beta;  // beta tiles per chunk
@@ -292,7 +298,7 @@ __device__ __forceinline__ void pass_tiles(const PassParams& p, const CUtensorMa
       return;
     }
     if (tid != 0) return;
-    if (pp.wait) pipe_wait(pp, (int)(t / pp.tpc));
+    if (PIPE && pp.wait) pipe_wait(pp, (int)(t / pp.tpc));
     if constexpr (ADJ) {
       mbar_expect_tx(&bars[s], (uint32_t)(W * N * sizeof(C)));
       for (int r0 = 0; r0 < N; r0 += ta.rows) {
@@ -373,9 +379,9 @@ __device__ __forceinline__ void pass_tiles(const PassParams& p, const CUtensorMa
 #if DFFTB_EXP_NOSTORE  // timing experiment only: compute without the global stores
     if (p.scale == 12345.0 && beta < p.B) store_lk<T, N, EPREF, LK>(p, sptr, v, j, alpha, beta, sc);
 #else
-    if (beta < p.B) store_lk<T, N, EPREF, LK>(p, sptr, v, j, alpha, beta, sc);
+    if (beta < p.B) store_lk<T, N, EPREF, LK, SPEC>(p, sptr, v, j, alpha, beta, sc);
 #endif
-    if (pp.npub) {
+    if (PIPE && pp.npub) {
       // producer: publish a chunk once this CTA has no further tile in it
       ++done;
       const int64_t c = t / pp.tpc;
@@ -398,13 +404,131 @@ __device__ __forceinline__ void pass_tiles(const PassParams& p, const CUtensorMa
   if constexpr (LK == kC2R) herm_reduce<T>(p.herm, lmax, limag);
 }
 
-template <typename T, int N, int EPREF, int W, bool ADJ, int STAGES, int LK>
+// The single-pass kernel.  Its body is the tile loop of pass_tiles written
+// out with blockIdx / gridDim (measured 1-2% faster than calling pass_tiles,
+// which the pipelined pair kernel below uses).  SPEC: the last forward pass of
+// a spectral operator (multiplier epilogue).
+template <typename T, int N, int EPREF, int W, bool ADJ, int STAGES, int LK, bool SPEC = false>
 __global__ void __launch_bounds__(W* Sched<N, EPREF>::TPL, DFFTB_TMA_MINB)
     fft_pass_tma_kernel(const __grid_constant__ PassParams p, const __grid_constant__ CUtensorMap tm,
                         const TmaArgs ta) {
+  using C = Cpx<T>;
+  using SC = Sched<N, EPREF>;
+  using TL = TmaLayout<T, N, W>;
+  constexpr int TPL = SC::TPL;
+  constexpr int LS = lane_stride<C>(N);
   extern __shared__ __align__(1024) unsigned char smem_tma[];
-  const PipeArgs pp{};  // single pass: natural tile order, no chunk protocol
-  pass_tiles<T, N, EPREF, W, ADJ, STAGES, LK>(p, tm, ta, pp, blockIdx.x, gridDim.x, smem_tma);
+  unsigned char* stg = smem_tma;
+  C* xch = reinterpret_cast<C*>(smem_tma + STAGES * TL::STG);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_tma + STAGES * TL::STG + TL::XCH);
+  void** sptr = reinterpret_cast<void**>(bars + STAGES);  // destination pointers
+
+  const int tid = threadIdx.x;
+  const int w = ADJ ? tid % W : tid / TPL;
+  const int j = ADJ ? tid / W : tid % TPL;
+  const int tiles_b = (p.B + W - 1) / W;
+  C* lane = xch + w * LS;
+  const C* tw = reinterpret_cast<const C*>(p.tw);
+  constexpr int ESIZE = LK == kR2C ? (int)sizeof(T) : (int)sizeof(C);
+  const T sc = static_cast<T>(p.scale);
+
+  // called by every thread; TMA ops are issued by thread 0 only
+  auto issue = [&](int64_t t, int s) {
+    const int alpha = (int)(t / tiles_b);
+    const int beta0 = (int)(t - (int64_t)alpha * tiles_b) * W;
+    unsigned char* dst = stg + s * TL::STG;
+    if (ADJ && ta.ldgsts) {
+      // very large row strides (e.g. the axis-0 pass) translate one page per
+      // row: spread the rows over all threads' LSU path instead of one TMA
+      // box walk.  Tile layout [i][w] as for TMA; lanes past B read as zero.
+      const C* src0 = reinterpret_cast<const C*>(p.in) + (int64_t)alpha * p.in_sa;
+      constexpr int NT = W * TPL;
+      for (int e = tid; e < W * N; e += NT) {
+        const int i = e / W, ww = e - (e / W) * W;
+        const bool ok = beta0 + ww < p.B;
+        const C* src = src0 + (int64_t)(ok ? beta0 + ww : 0) * p.in_sb + (int64_t)i * p.in_si;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst + (size_t)e * sizeof(C))),
+                     "l"(src), "r"(ok ? 16 : 0)
+                     : "memory");
+      }
+      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&bars[s])) : "memory");
+      return;
+    }
+    if (tid != 0) return;
+    if constexpr (ADJ) {
+      mbar_expect_tx(&bars[s], (uint32_t)(W * N * sizeof(C)));
+      for (int r0 = 0; r0 < N; r0 += ta.rows) {
+        const int c1 = ta.i_dim == 1 ? r0 : alpha;
+        const int c2 = ta.i_dim == 1 ? alpha : r0;
+        tma_load_3d(dst + (size_t)r0 * W * sizeof(C), &tm, 2 * beta0, c1, c2, &bars[s]);
+      }
+    } else {
+      const int nvalid = min(W, p.B - beta0);
+      const uint32_t bytes = (uint32_t)nvalid * (uint32_t)ta.lane_bytes;
+      mbar_expect_tx(&bars[s], bytes);
+      const unsigned char* src = reinterpret_cast<const unsigned char*>(p.in) +
+                                 (in_alpha_off(p, alpha) + (int64_t)beta0 * p.in_sb) * ESIZE;
+      bulk_load(dst, src, bytes, &bars[s]);
+    }
+  };
+
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], (ADJ && ta.ldgsts) ? W * TPL : 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (tid < kMaxDest) sptr[tid] = p.dest[tid].ptr;
+  __syncthreads();
+  for (int s = 0; s < STAGES; ++s) {
+    const int64_t t = blockIdx.x + (int64_t)s * gridDim.x;
+    if (t < ta.ntiles) issue(t, s);
+  }
+
+  T lmax = T(0), limag = T(0);  // C2R statistics, reduced once per CTA at the end
+  int k = 0;
+  for (int64_t t = blockIdx.x; t < ta.ntiles; t += gridDim.x, ++k) {
+    const int s = k % STAGES;
+    mbar_wait(&bars[s], (uint32_t)((k / STAGES) & 1));
+    const int alpha = (int)(t / tiles_b);
+    const int beta = (int)(t - (int64_t)alpha * tiles_b) * W + w;
+    const unsigned char* st = stg + s * TL::STG;
+    C v[SC::E];
+    if constexpr (ADJ) {
+      const C* scp = reinterpret_cast<const C*>(st);
+      fetch0_lk<T, N, EPREF, LK>(
+          v, j, [&](int pos) { return scp[pos * W + w]; }, [&](int) { return T(0); });
+    } else {
+      const int ll = ta.lane_bytes / ESIZE;  // stored lane length in elements
+      const C* scp = reinterpret_cast<const C*>(st) + w * ll;
+      const T* srp = reinterpret_cast<const T*>(st) + w * ll;
+      fetch0_lk<T, N, EPREF, LK>(
+          v, j, [&](int pos) { return scp[pos]; }, [&](int pos) { return srp[pos]; });
+    }
+    if constexpr (LK == kC2R) {
+      // NonHermitian statistics straight from the staged half spectrum:
+      // block max |X| and the DC / Nyquist imaginary residues of active lanes
+      if (beta < p.B) {
+        const int ll = ta.lane_bytes / ESIZE;
+        const C* scp = reinterpret_cast<const C*>(st) + w * ll;
+        for (int i = j; i <= N / 2; i += TPL) {  // stored bins only, not the row padding
+          const C x = scp[i];
+          const T m = sqrt(x.x * x.x + x.y * x.y);
+          lmax = m > lmax ? m : lmax;
+          if (i == 0 || i == N / 2) limag = fabs(x.y) > limag ? fabs(x.y) : limag;
+        }
+      }
+    }
+    __syncthreads();  // staging slot s fully consumed by every thread
+    {
+      const int64_t t2 = t + (int64_t)STAGES * gridDim.x;
+      if (t2 < ta.ntiles) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(t2, s);
+      }
+    }
+    run_stages<T, N, EPREF, 0>(v, lane, tw, j);
+    if (beta < p.B) store_lk<T, N, EPREF, LK, SPEC>(p, sptr, v, j, alpha, beta, sc);
+  }
+  if constexpr (LK == kC2R) herm_reduce<T>(p.herm, lmax, limag);
 }
 
 // Pipelined pair: CTAs [0, ncta_a) run the producer pass, the rest the
@@ -418,10 +542,10 @@ __global__ void __launch_bounds__(W* Sched<N, EPREF>::TPL, DFFTB_TMA_MINB)
                     const __grid_constant__ TmaArgs tab, const __grid_constant__ PipeArgs ppb, int ncta_a) {
   extern __shared__ __align__(1024) unsigned char smem_tma[];
   if ((int)blockIdx.x < ncta_a)
-    pass_tiles<T, N, EPREF, W, ADJ_A, STAGES, LK>(pa, tma, taa, ppa, blockIdx.x, ncta_a, smem_tma);
+    pass_tiles<T, N, EPREF, W, ADJ_A, STAGES, LK, false, true>(pa, tma, taa, ppa, blockIdx.x, ncta_a, smem_tma);
   else
-    pass_tiles<T, N, EPREF, W, ADJ_B, STAGES, LK>(pb, tmb, tab, ppb, blockIdx.x - ncta_a,
-                                                   gridDim.x - ncta_a, smem_tma);
+    pass_tiles<T, N, EPREF, W, ADJ_B, STAGES, LK, false, true>(pb, tmb, tab, ppb, blockIdx.x - ncta_a,
+                                                                gridDim.x - ncta_a, smem_tma);
 }
 
 }  // namespace dfftb

@@ -93,10 +93,10 @@ struct TmaCfg {
   static constexpr int SMEM = STAGES * TL::STG + TL::XCH + 8 * STAGES + 8 * kMaxDest;
 };
 
-template <typename T, int N, bool ADJ, int LK>
+template <typename T, int N, bool ADJ, int LK, bool SPEC = false>
 static cudaError_t launch_tma_tn(const PassParams& p, const TmaPlan& tp, cudaStream_t s) {
   using Cf = TmaCfg<T, N>;
-  auto kern = fft_pass_tma_kernel<T, N, Cf::EPREF, Cf::W, ADJ, Cf::STAGES, LK>;
+  auto kern = fft_pass_tma_kernel<T, N, Cf::EPREF, Cf::W, ADJ, Cf::STAGES, LK, SPEC>;
   static int grid_cap[64] = {0};
   int dev = 0;
   cudaGetDevice(&dev);
@@ -124,6 +124,7 @@ static cudaError_t launch_tma_prec(int n, const PassParams& p, bool adj, const T
 #define DFFTB_TMA_CASE(NN)                                                \
   case NN:                                                                \
     if (adj) {                                                            \
+      if (lk == kC2CFwd && p.spec.op) return launch_tma_tn<T, NN, true, kC2CFwd, true>(p, tp, s); \
       if (lk == kC2CFwd) return launch_tma_tn<T, NN, true, kC2CFwd>(p, tp, s);  \
       if (lk == kC2CBwd) return launch_tma_tn<T, NN, true, kC2CBwd>(p, tp, s);  \
       return cudaErrorInvalidValue;                                       \

@@ -3,7 +3,10 @@
 Mirror of the reference's SpectralContext / derivative / gradient /
 divergence / laplacian / inverse_laplacian.  The forward and backward
 transforms are the B200 execute path; the i*k and -|k|^2 multipliers run as
-one device kernel over this rank's frequency block (dfftb_spectral_apply).
+one device kernel over this rank's frequency block (dfftb_spectral_apply),
+or — the default for the operators below — inside the store epilogue of the
+forward transform's last pass (dfftb_execute_spectral: one pass over the
+spectrum less, bit-identical values).
 """
 from __future__ import annotations
 
@@ -87,6 +90,26 @@ class SpectralContext:
                                                    1 if accumulate else 0, stream))
 
 
+    def _forward_op(self, fwd: Plan, op, axis, x: DistTensor, out: Optional[DistTensor] = None,
+                    accumulate=False) -> DistTensor:
+        """out (+)= op(forward(x)) with the multiplier fused into the forward's
+        last pass (dfftb_execute_spectral)."""
+        if x.dist != fwd.input:
+            raise Error(17, "input layout differs from the plan's")
+        if out is None:
+            out = DistTensor(fwd.output, x.rank,
+                             torch.empty(fwd.output.local_count(x.rank), dtype=fwd.dtype_of(fwd.output),
+                                         device=x.data.device))
+        nd = len(self.dims)
+        lens = _lengths(self.domain_lengths, nd)
+        xd = x.data if x.data.is_contiguous() else x.data.contiguous()
+        stream = torch.cuda.current_stream(x.data.device).cuda_stream
+        with torch.cuda.device(x.data.device):
+            _check(_lib.lib().dfftb_execute_spectral(fwd._h, self.exec._h, xd.data_ptr(), out.data.data_ptr(),
+                                                     op, axis, lens, 1 if accumulate else 0, stream, 0))
+        return out
+
+
 def make_spectral_context(dims, grid, domain_lengths=None, precision="f64", comm=None, rank=None,
                           decomp="pencil") -> SpectralContext:
     return SpectralContext(dims, grid, domain_lengths, precision, comm, rank, decomp)
@@ -96,8 +119,7 @@ def derivative(ctx: SpectralContext, x: DistTensor, axis: int) -> DistTensor:
     """backward(i k_axis (.) forward(x)), normalized (spectral.hpp:131-164)."""
     from .dfft import execute
     fwd, bwd = ctx._plans(x)
-    spec = execute(fwd, x, ctx.exec)
-    ctx._apply(fwd, DERIV, axis, spec, spec)
+    spec = ctx._forward_op(fwd, DERIV, axis, x)
     return execute(bwd, spec, ctx.exec)
 
 
@@ -114,12 +136,7 @@ def divergence(ctx: SpectralContext, components: Sequence[DistTensor]) -> DistTe
     fwd, bwd = ctx._plans(components[0])
     acc = None
     for a, c in enumerate(components):
-        spec = execute(fwd, c, ctx.exec)
-        if acc is None:
-            acc = spec
-            ctx._apply(fwd, DERIV, a, spec, acc)
-        else:
-            ctx._apply(fwd, DERIV, a, spec, acc, accumulate=True)
+        acc = ctx._forward_op(fwd, DERIV, a, c, out=acc, accumulate=acc is not None)
     return execute(bwd, acc, ctx.exec)
 
 
@@ -127,8 +144,7 @@ def laplacian(ctx: SpectralContext, x: DistTensor) -> DistTensor:
     """backward(-|k|^2 (.) forward(x)), normalized (spectral.hpp:219-249)."""
     from .dfft import execute
     fwd, bwd = ctx._plans(x)
-    spec = execute(fwd, x, ctx.exec)
-    ctx._apply(fwd, LAPLACIAN, 0, spec, spec)
+    spec = ctx._forward_op(fwd, LAPLACIAN, 0, x)
     return execute(bwd, spec, ctx.exec)
 
 
@@ -137,6 +153,5 @@ def inverse_laplacian(ctx: SpectralContext, x: DistTensor) -> DistTensor:
     field has zero mean (spectral.hpp:251-309)."""
     from .dfft import execute
     fwd, bwd = ctx._plans(x)
-    spec = execute(fwd, x, ctx.exec)
-    ctx._apply(fwd, INV_LAPLACIAN, 0, spec, spec)
+    spec = ctx._forward_op(fwd, INV_LAPLACIAN, 0, x)
     return execute(bwd, spec, ctx.exec)

@@ -43,6 +43,21 @@ def cases(P):
             ("slab", [32, 32, 32], [P], "c2c", "f64")]
 
 
+def fused_spectral_matches(fwd, ctx, x, rank):
+    lib = D._lib.lib()
+    stream = torch.cuda.current_stream().cuda_stream
+    n = fwd.output.local_count(rank)
+    fused = torch.zeros(n, dtype=fwd.dtype_of(fwd.output), device="cuda")
+    D.dfft._check(lib.dfftb_execute_spectral(fwd._h, ctx._h, x.data.data_ptr(), fused.data_ptr(), 1, 0,
+                                             None, 0, stream, 1))
+    spec = D.execute(fwd, x, ctx)
+    unf = torch.zeros_like(fused)
+    D.dfft._check(lib.dfftb_spectral_apply(fwd._h, rank, 1, 0, None, spec.data.data_ptr(), unf.data_ptr(), 0,
+                                           stream))
+    torch.cuda.synchronize()
+    return bool(torch.equal(fused, unf))
+
+
 def gather_global(dist_, block, rank, world):
     blocks = [None] * world
     dist.all_gather_object(blocks, block.data.cpu().numpy())
@@ -85,6 +100,24 @@ def main():
             ok = ok and good
             print(f"{'ok  ' if good else 'FAIL'} {decomp} {dims} grid {grid} {kind} {prec}: "
                   f"fwd vs oracle {e_f:.2e}, round trip {e_r:.2e}", flush=True)
+        # fused spectral epilogue == execute + spectral_apply, on every rank
+        spec_ok = fused_spectral_matches(fwd, ctx, x, rank)
+        # the (opt-in) pipelined pass pairs give bit-identical blocks
+        os.environ["DFFTB_PIPE"] = "1"
+        for _ in range(2):
+            yp = D.execute(fwd, x, ctx)
+            zp = D.execute(bwd, yp, ctx)
+        torch.cuda.synchronize()
+        ctx.check()
+        del os.environ["DFFTB_PIPE"]
+        pipe_ok = bool(torch.equal(yp.data, y.data)) and bool(torch.equal(zp.data, z.data))
+        flags = torch.tensor([1 if spec_ok else 0, 1 if pipe_ok else 0], device="cuda")
+        dist.all_reduce(flags, op=dist.ReduceOp.MIN)
+        if rank == 0:
+            good = bool(flags[0].item() == 1 and flags[1].item() == 1)
+            ok = ok and good
+            print(f"{'ok  ' if good else 'FAIL'}   fused spectral epilogue {bool(flags[0].item())}, "
+                  f"pipelined pairs bit-identical {bool(flags[1].item())}", flush=True)
         ctx.close()
         dist.barrier()
     flag = torch.tensor([1 if ok else 0], device="cuda")

@@ -138,3 +138,83 @@ def test_spectral_on_emulated_world():
     zs = D.execute_world(bwd, ys, ctxs)
     got = gather(bwd.output, zs)
     assert np.max(np.abs(got - (-3j) * f)) < 1e-10
+
+
+def _spectral_pair(plan, ctx, x, op, axis, lens=None, accumulate_into=None):
+    """(fused, unfused) spectra of op(forward(x)) for one rank."""
+    import ctypes
+    lib = D._lib.lib()
+    nd = len(plan.dims)
+    cl = (ctypes.c_double * nd)(*lens) if lens else None
+    stream = torch.cuda.current_stream().cuda_stream
+    n = plan.output.local_count(0)
+    fused = torch.zeros(n, dtype=plan.dtype_of(plan.output), device="cuda")
+    if accumulate_into is not None:
+        fused.copy_(accumulate_into)
+    D.dfft._check(lib.dfftb_execute_spectral(plan._h, ctx._h, x.data.data_ptr(), fused.data_ptr(), op, axis,
+                                             cl, 1 if accumulate_into is not None else 0, stream, 1))
+    spec = D.execute(plan, x, ctx)
+    unf = torch.zeros_like(fused)
+    if accumulate_into is not None:
+        unf.copy_(accumulate_into)
+    D.dfft._check(lib.dfftb_spectral_apply(plan._h, 0, op, axis, cl, spec.data.data_ptr(), unf.data_ptr(),
+                                           1 if accumulate_into is not None else 0, stream))
+    torch.cuda.synchronize()
+    return fused.cpu(), unf.cpu()
+
+
+FUSED_CASES = [
+    ("pencil", (32, 16, 64), (1, 1), "c2c", "f64"),
+    ("pencil", (32, 16, 64), (1, 1), "r2c", "f64"),
+    ("slab", (64, 32, 16), (1,), "c2c", "f32"),
+    ("pencil", (16, 32, 32), (1, 1), "r2c", "f32"),
+    ("pencil", (24, 20, 16), (1, 1), "c2c", "f64"),   # non-pow2: two-step fallback
+    ("slab", (64, 32), (1,), "c2c", "f64"),           # 2-D
+    ("general", (8, 8, 16, 16), (1, 1, 1), "c2c", "f64"),  # 4-D
+]
+
+
+@gpu
+@pytest.mark.parametrize("decomp,dims,grid,kind,prec", FUSED_CASES)
+def test_fused_spectral_epilogue_matches_two_step(decomp, dims, grid, kind, prec):
+    """dfftb_execute_spectral (multiplier in the last forward pass's store)
+    is bit-identical to execute + dfftb_spectral_apply."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    k = D.TransformKind.R2C if kind == "r2c" else D.TransformKind.C2C
+    mk = {"pencil": D.plan_pencil, "general": D.plan_general}.get(decomp)
+    if decomp == "slab":
+        plan = D.plan_slab(dims, grid[0], k, D.Direction.Forward, precision=prec)
+    else:
+        plan = mk(dims, grid, k, D.Direction.Forward, precision=prec)
+    ctx = D.make_context(plan)
+    x = D.DistTensor.seeded(plan.input, 0, complex_field=kind == "c2c")
+    lens = [1.0 + a for a in range(len(dims))]
+    for op, axis in [(S.DERIV, a) for a in range(len(dims))] + [(S.LAPLACIAN, 0)]:
+        f, u = _spectral_pair(plan, ctx, x, op, axis, lens)
+        assert torch.equal(f, u), (op, axis)
+    # accumulate (divergence) into an existing spectrum
+    base = D.execute(plan, x, ctx).data.clone()
+    f, u = _spectral_pair(plan, ctx, x, S.DERIV, len(dims) - 1, lens, accumulate_into=base)
+    assert torch.equal(f, u)
+    if prec == "f32":
+        return  # a float32 field cannot be made zero-mean to 1e-12 N
+    # inverse Laplacian of a zero-mean field
+    xm = D.DistTensor(plan.input, 0, x.data - x.data.mean())
+    f, u = _spectral_pair(plan, ctx, xm, S.INV_LAPLACIAN, 0, lens)
+    assert torch.equal(f, u)
+
+
+@gpu
+def test_fused_inverse_laplacian_nonzero_mean():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    plan = D.plan_pencil((16, 16, 16), (1, 1), D.TransformKind.C2C, D.Direction.Forward)
+    ctx = D.make_context(plan)
+    x = D.DistTensor(plan.input, 0, torch.ones(16 ** 3, dtype=torch.complex128, device="cuda"))
+    out = torch.empty_like(x.data)
+    import ctypes
+    st = D._lib.lib().dfftb_execute_spectral(plan._h, ctx._h, x.data.data_ptr(), out.data_ptr(),
+                                             S.INV_LAPLACIAN, 0, None, 0,
+                                             torch.cuda.current_stream().cuda_stream, 1)
+    assert D._lib.lib().dfftb_error_name(st).decode() == "NonZeroMean"

@@ -48,6 +48,9 @@
 #ifndef DFFTB_EXP_NOSTORE
 #define DFFTB_EXP_NOSTORE 0  // timing experiment: skip the global stores
 #endif
+#ifndef DFFTB_TWB
+#define DFFTB_TWB 1  // twiddle bases kept in registers across tiles
+#endif
 #ifndef DFFTB_TMA_MINB
 #define DFFTB_TMA_MINB 1    // resident CTAs per SM the TMA kernel is compiled for
 #endif
@@ -300,11 +303,41 @@ __device__ __forceinline__ unsigned long long dbits(T v) {
   return static_cast<unsigned long long>(__double_as_longlong(static_cast<double>(v)));
 }
 
+// This thread's twiddle bases, one per (stage >= 1, butterfly).  They depend
+// on the thread's position j only, not on the tile, so persistent kernels load
+// them once and keep them in registers (no table read on the tile path).
+template <typename T, int N, int EPREF>
+struct TwBase {
+  using SC = Sched<N, EPREF>;
+  __host__ __device__ static constexpr int off(int s) { return s <= 1 ? 0 : off(s - 1) + SC::E / SC::radix(s - 1); }
+  static constexpr int COUNT = SC::S <= 1 ? 1 : off(SC::S);
+  Cpx<T> w[COUNT];
+};
+
+template <typename T, int N, int EPREF, int s = 1>
+__device__ __forceinline__ void load_twbase(TwBase<T, N, EPREF>& b, const Cpx<T>* tw, int j) {
+  using SC = Sched<N, EPREF>;
+  if constexpr (s < SC::S) {
+    constexpr int R = SC::radix(s);
+    constexpr int NS = SC::ns(s);
+    constexpr int NB = SC::E / R;
+#pragma unroll
+    for (int t = 0; t < NB; ++t) {
+      const int bidx = j + t * SC::TPL;
+      const int pp = bidx & (NS - 1);
+      b.w[TwBase<T, N, EPREF>::off(s) + t] = __ldg(tw + pp * (N / (NS * R)));
+    }
+    load_twbase<T, N, EPREF, s + 1>(b, tw, j);
+  }
+}
+
 // Stage s of the self-sorting Stockham schedule (compile-time recursion so
 // every register index is static).  On entry v holds this thread's inputs of
-// stage s: slot t*R+r = position (j + t*TPL) + r*N/R.
+// stage s: slot t*R+r = position (j + t*TPL) + r*N/R.  twb: preloaded
+// twiddle bases (nullptr: read the table).
 template <typename T, int N, int EPREF, int s>
-__device__ __forceinline__ void run_stages(Cpx<T>* v, Cpx<T>* lane, const Cpx<T>* tw, int j) {
+__device__ __forceinline__ void run_stages(Cpx<T>* v, Cpx<T>* lane, const Cpx<T>* tw, int j,
+                                           const TwBase<T, N, EPREF>* twb = nullptr) {
   using C = Cpx<T>;
   using SC = Sched<N, EPREF>;
   if constexpr (s < SC::S) {
@@ -323,7 +356,7 @@ __device__ __forceinline__ void run_stages(Cpx<T>* v, Cpx<T>* lane, const Cpx<T>
         // one table read per butterfly, the other powers by products
         // (depth <= 3 multiplications: a few ulp, far inside 1e-12)
         C wp[R];
-        wp[1] = __ldg(tw + step);
+        wp[1] = twb ? twb->w[TwBase<T, N, EPREF>::off(s) + t] : __ldg(tw + step);
 #pragma unroll
         for (int r = 2; r < R; ++r) wp[r] = cmul(wp[r / 2], wp[r - r / 2]);
 #pragma unroll
@@ -354,7 +387,7 @@ __device__ __forceinline__ void run_stages(Cpx<T>* v, Cpx<T>* lane, const Cpx<T>
 #pragma unroll
         for (int r = 0; r < R2; ++r) v[t * R2 + r] = lane[spad<C>(j + t * TPL + r * (N / R2))];
       }
-      run_stages<T, N, EPREF, s + 1>(v, lane, tw, j);
+      run_stages<T, N, EPREF, s + 1>(v, lane, tw, j, twb);
     }
   }
 }

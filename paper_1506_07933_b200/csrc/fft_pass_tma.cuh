@@ -431,6 +431,13 @@ __global__ void __launch_bounds__(W* Sched<N, EPREF>::TPL, DFFTB_TMA_MINB)
   const C* tw = reinterpret_cast<const C*>(p.tw);
   constexpr int ESIZE = LK == kR2C ? (int)sizeof(T) : (int)sizeof(C);
   const T sc = static_cast<T>(p.scale);
+#if DFFTB_TWB
+  TwBase<T, N, EPREF> twb;  // per-thread twiddle bases, loaded once per kernel
+  load_twbase<T, N, EPREF>(twb, tw, j);
+  const TwBase<T, N, EPREF>* twbp = &twb;
+#else
+  const TwBase<T, N, EPREF>* twbp = nullptr;
+#endif
 
   // called by every thread; TMA ops are issued by thread 0 only
   auto issue = [&](int64_t t, int s) {
@@ -525,7 +532,7 @@ __global__ void __launch_bounds__(W* Sched<N, EPREF>::TPL, DFFTB_TMA_MINB)
         issue(t2, s);
       }
     }
-    run_stages<T, N, EPREF, 0>(v, lane, tw, j);
+    run_stages<T, N, EPREF, 0>(v, lane, tw, j, twbp);
     if (beta < p.B) store_lk<T, N, EPREF, LK, SPEC>(p, sptr, v, j, alpha, beta, sc);
   }
   if constexpr (LK == kC2R) herm_reduce<T>(p.herm, lmax, limag);

@@ -46,6 +46,20 @@ __global__ void peer_store_smem(double2* __restrict__ dst, const double2* __rest
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) dst[i] = src[i];
 }
 
+// 128-byte segments at a large stride (the fused exchange pass's store
+// pattern: 8 lanes x 16 B per transformed index, rows `stride` apart)
+__global__ void peer_store_seg(double2* __restrict__ dst, size_t n, size_t seg_elems, size_t stride_elems) {
+  const size_t nseg = n / seg_elems;
+  const size_t rows = stride_elems / seg_elems;  // segments per row
+  const size_t nrows = nseg / rows;
+  const size_t gstride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gstride) {
+    const size_t s = i / seg_elems, e = i - s * seg_elems;
+    const size_t r = s % nrows, c = s / nrows;  // consecutive segments go to different rows
+    dst[r * stride_elems + c * seg_elems + e] = make_double2((double)i, 0.0);
+  }
+}
+
 int main() {
   int n = 0;
   cudaGetDeviceCount(&n);
@@ -105,6 +119,35 @@ int main() {
                            : "TMA bulk local stores",
                bytes / (worst * 1e-3) / 1e9, n);
     }
+  }
+  for (int segb = 128; segb <= 2048; segb *= 4) {
+    const size_t seg = segb / 16, stride = 512 * 1024 / 16;  // 512 KB between rows
+    float worst = 0;
+    for (int rep = 0; rep < 3; ++rep) {
+      std::vector<cudaEvent_t> e0(n), e1(n);
+      for (int d = 0; d < n; ++d) {
+        cudaSetDevice(d);
+        cudaDeviceSynchronize();
+        cudaEventCreate(&e0[d]);
+        cudaEventCreate(&e1[d]);
+      }
+      for (int d = 0; d < n; ++d) {
+        cudaSetDevice(d);
+        cudaEventRecord(e0[d]);
+        peer_store_seg<<<148 * 4, 512>>>(buf[(d + 1) % n], elems, seg, stride);
+        cudaEventRecord(e1[d]);
+      }
+      worst = 0;
+      for (int d = 0; d < n; ++d) {
+        cudaSetDevice(d);
+        cudaEventSynchronize(e1[d]);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0[d], e1[d]);
+        worst = ms > worst ? ms : worst;
+      }
+    }
+    printf("peer stores in %d-byte segments, 512 KB row stride: %.0f GB/s per GPU\n", segb,
+           bytes / (worst * 1e-3) / 1e9);
   }
   // overlap check: peer-store kernel and local-copy kernel on disjoint SM
   // halves (1 CTA per SM forced by shared memory), concurrently

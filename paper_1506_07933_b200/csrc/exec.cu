@@ -490,7 +490,8 @@ static bool plan_tma(Op& op, int prec) {
       // strides) or per-thread cp.async (DFFTB_ADJ_LOADER=ldgsts|auto)
       const char* e = getenv("DFFTB_ADJ_LOADER");
       const std::string mode = e ? e : "tma";
-      tp.args.ldgsts = mode == "ldgsts" || (mode == "auto" && si >= (int64_t(1) << 20));
+      // (16-byte cp.async per element: fp64 complex only)
+      tp.args.ldgsts = csize == 16 && (mode == "ldgsts" || (mode == "auto" && si >= (int64_t(1) << 20)));
       if (tp.args.ldgsts) return true;
     }
     auto enc = tensor_map_encoder();

@@ -1177,6 +1177,18 @@ static void run_program(const Plan& plan, Ctx& ctx, const std::vector<Op>& prog,
     float ms = 0;
     cudaEventElapsedTime(&ms, et.ev.front(), et.ev.back());
     timers->total = ms * 1e-3;
+    // profiling aid: DFFTB_OP_TIMES=1 prints every op of the program
+    const char* ot = getenv("DFFTB_OP_TIMES");
+    if (ot && *ot == '1') {
+      for (size_t k = 0; k < prog.size(); ++k) {
+        float m = 0;
+        cudaEventElapsedTime(&m, et.ev[k], et.ev[k + 1]);
+        const Op& o = prog[k];
+        fprintf(stderr, "[dfftb rank %d] op %zu %s n=%d A=%d B=%d dests=%d: %.3f ms\n", ctx.rank, k,
+                o.barrier ? "barrier" : (o.pipe ? "pipe" : (o.fused ? "fused-exchange" : "local")), o.n, o.p.A,
+                o.p.B, o.p.ndest, m);
+      }
+    }
   }
   if (timers || (flags & DFFTB_EXEC_SYNC)) ctx_check(ctx, s);
 }

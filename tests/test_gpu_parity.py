@@ -228,3 +228,69 @@ def test_512_cubed_single_gpu_properties():
                         k[a] / 512) for a in range(3)]
         val = torch.einsum("ijk,i,j,k->", xg, ph[0], ph[1], ph[2]).item()
         assert abs(yb[k].item() - val) <= 1e-10 * np.sqrt(freq / n)
+
+
+def _spot_bins(xg, yb, dims, bins, half_last=False):
+    """Largest |y[k] - direct double DFT sum| over the given bins, and the
+    RMS spectrum magnitude for scale."""
+    dev = xg.device
+    worst = 0.0
+    for k in bins:
+        ph = [torch.exp(-2j * np.pi * torch.arange(dims[a], device=dev, dtype=torch.float64) * k[a] / dims[a])
+              for a in range(3)]
+        val = torch.einsum("ijk,i,j,k->", xg.to(torch.complex128), ph[0], ph[1], ph[2]).item()
+        worst = max(worst, abs(complex(yb[k].item()) - val))
+    return worst
+
+
+def test_config_D_1024_cubed_properties():
+    # BASELINE config D (1024^3 C2C fp64) at full size on one GPU: round trip,
+    # Parseval and direct-DFT spot bins (the oracle would need ~92 GB of RAM)
+    dims = [1024, 1024, 1024]
+    fwd = make_plan("pencil", dims, [1, 1], "c2c", "forward")
+    bwd = make_plan("pencil", dims, [1, 1], "c2c", "backward")
+    ctx = D.make_context(fwd)
+    x = D.DistTensor.seeded(fwd.input, 0)
+    y = D.execute(fwd, x, ctx)
+    z = D.execute(bwd, y, ctx)
+    xd = x.data
+    assert (torch.linalg.vector_norm(z.data - xd) / torch.linalg.vector_norm(xd)).item() < 1e-14
+    del z
+    n = xd.numel()
+    space = torch.sum(torch.abs(xd) ** 2).item()
+    freq = torch.sum(torch.abs(y.data) ** 2).item()
+    assert abs(n * space - freq) <= 1e-12 * freq
+    err = _spot_bins(xd.view(dims), y.data.view(dims), dims, [(0, 0, 0), (1023, 5, 512), (300, 700, 9)])
+    assert err <= 1e-10 * np.sqrt(freq / n)
+    ctx.close()
+
+
+def test_config_E_r2c_f32_properties():
+    # BASELINE config E (2048x512x256 R2C -> C2R fp32) at full size: round trip
+    # within the fp32 tolerance and spot bins against a double direct sum
+    dims = [2048, 512, 256]
+    fwd = make_plan("pencil", dims, [1, 1], "r2c", "forward", "f32")
+    bwd = make_plan("pencil", dims, [1, 1], "c2r", "backward", "f32")
+    ctx = D.make_context(fwd)
+    x = D.DistTensor.seeded(fwd.input, 0, complex_field=False)
+    y = D.execute(fwd, x, ctx)
+    z = D.execute(bwd, y, ctx)
+    xd = x.data
+    assert (torch.linalg.vector_norm(z.data - xd) / torch.linalg.vector_norm(xd)).item() < 1e-5
+    hd = [2048, 512, 129]
+    yb = y.data.view(hd)
+    n = xd.numel()
+    rms = np.sqrt(n * torch.sum(xd.double() ** 2).item())  # |X| scale (Parseval)
+    err = _spot_bins(xd.view(dims), yb, dims, [(0, 0, 0), (2047, 3, 128), (1000, 255, 77)])
+    assert err <= 1e-5 * rms / np.sqrt(n) * 10
+    ctx.close()
+
+
+def test_config_B_256_r2c_against_oracle():
+    # BASELINE config B (256^3 R2C f64, slab P=1) against the C oracle at full size
+    dims = [256, 256, 256]
+    xg = O.seeded(dims, False, "f64")
+    y_ref, _ = O.execute(xg, dims, "slab", [1], "r2c", "forward", "f64")
+    fwd = make_plan("slab", dims, [1], "r2c", "forward")
+    y = run_world(fwd, xg)
+    assert rel_l2(y, y_ref) <= 1e-12

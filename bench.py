@@ -332,7 +332,7 @@ def main():
             e2e_step(i)
         barrier()
         ev.clear()
-        Ke = max(4, min(K, 16))   # amortise the pipeline fill (first upload, last download)
+        Ke = max(16, min(K, 32))  # amortise the pipeline fill (first upload, last download)
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record(s_in)

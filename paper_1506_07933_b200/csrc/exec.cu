@@ -334,6 +334,8 @@ void ctx_destroy(Ctx* ctx) {
     cudaFree(ctx->work);
     cudaFree(ctx->dstat);
     if (ctx->fuse_ring) cudaFree(ctx->fuse_ring);
+    if (ctx->ring) cudaFree(ctx->ring);
+    if (ctx->ring_ctr) cudaFree(ctx->ring_ctr);
     if (ctx->fuse_counters) cudaFree(ctx->fuse_counters);
     cudaGetLastError();
   }
@@ -385,6 +387,7 @@ struct Op {
   TmaPlan tpb{};
   PipeArgs ppa{}, ppb{};
   double frac = 0.5;
+  bool ring_reset = false;  // zero the ring counters before the launch
 };
 
 // Row-major element strides of a block; internal buffers pad the innermost
@@ -916,12 +919,148 @@ static void pipeline_pairs(std::vector<Op>& prog, Ctx& ctx) {
   }
 }
 
+// Single GPU: the rows pass and the columns pass of every x0 plane run as
+// ONE pipelined launch whose intermediate lives in an L2-resident ring of
+// planes instead of a full buffer in HBM — two axes for one HBM round trip.
+// Producer CTAs transform rows into ring slot (plane % ring); consumer CTAs
+// wait for a chunk of planes, load it (TMA), drop the ring rows from L2
+// (discard: never written back) and transform the columns; the producer
+// reuses a slot once its chunk was consumed.  Counters are local and zeroed
+// before each launch (stream order), so no cross-execute bookkeeping.
+static constexpr int kRingMaxChunks = 4096;
+
+static bool ring_enabled() {
+  const char* e = getenv("DFFTB_RING");
+  return e && *e == '1';
+}
+
+static void ring_pairs(std::vector<Op>& prog, Ctx& ctx) {
+  if (ctx.world_mode || ctx.nranks != 1 || prog.size() < 2 || !ring_enabled()) return;
+  Op& P = prog[0];
+  Op& Q = prog[1];
+  const int prec = ctx.prec;
+  const int64_t csize = 2 * prec;
+  auto plain = [&](const Op& o) {
+    return !o.barrier && o.tma && !o.generic && !o.fused2 && !o.pipe && o.p.in_mode == kInComplex &&
+           !o.p.out_real && o.p.A1 <= 1 && o.p.A > 0 && o.p.B > 0 && !o.tp.args.ldgsts;
+  };
+  if (!plain(P) || !plain(Q) || P.n != Q.n || !pipe_supported(prec, P.n)) return;
+  if (P.adj || !Q.adj || P.p.inverse != Q.p.inverse) return;
+  if (P.p.ndest != 1 || P.p.store_mode != 0 || P.p.dest[0].ptr != Q.p.in) return;
+  if (P.p.A != Q.p.A || P.p.dest[0].sa != Q.p.in_sa || P.p.dest[0].base != 0 || Q.p.in_sb != 1) return;
+  const int W = tma_tile_w(prec, P.n);
+  int R = 2, L = 4;
+  if (const char* e = getenv("DFFTB_RING_R")) R = std::max(1, atoi(e));
+  if (const char* e = getenv("DFFTB_RING_L")) L = std::max(2, atoi(e));
+  double frac = 0.5;
+  if (const char* e = getenv("DFFTB_RING_FRAC")) frac = atof(e);
+  // Deadlock freedom: a CTA waits (for its prefetch, STAGES tiles ahead)
+  // while holding its current tiles unstored.  The producer's reuse lag must
+  // therefore exceed both roles' prefetch reach in chunks.
+  {
+    const int64_t tb = std::max<int64_t>((P.p.B + W - 1) / W, (Q.p.B + W - 1) / W);
+    const int np = std::max(1, (int)(frac * 148 + 0.5)), nq = std::max(1, 148 - np);
+    const int64_t reach = 2 * (int64_t)std::max(np, nq);  // STAGES = 2 tiles per CTA ahead
+    R = std::max<int64_t>(R, (reach + tb - 1) / tb);       // a chunk spans one reach
+    const int64_t tpc = (int64_t)R * ((std::min(P.p.B, Q.p.B) + W - 1) / W);
+    const int need = (int)((reach + tpc - 1) / tpc) * 2 + 2;
+    L = std::max(L, need);
+  }
+  const int A = P.p.A;
+  const int ringP = R * L;
+  const int C = (A + R - 1) / R;
+  if (A < 2 * ringP || C > kRingMaxChunks) return;
+  const size_t bytes = (size_t)ringP * (size_t)Q.p.in_sa * csize;
+  if (ctx.ring_bytes < bytes) {
+    if (ctx.ring) cudaFree(ctx.ring);
+    ctx.ring = nullptr;
+    ctx.ring_bytes = 0;
+    CUDA_TRY(cudaMalloc(&ctx.ring, bytes));
+    ctx.ring_bytes = bytes;
+  }
+  if (!ctx.ring_ctr) CUDA_TRY(cudaMalloc(&ctx.ring_ctr, 2 * kRingMaxChunks * sizeof(unsigned long long)));
+  // consumer's tensor map over the ring (same strides, ringP planes)
+  TmaPlan tq = Q.tp;
+  {
+    auto enc = tensor_map_encoder();
+    if (!enc) return;
+    const int64_t si = Q.p.in_si * csize, sa = Q.p.in_sa * csize;
+    cuuint64_t gdim[3] = {2 * (cuuint64_t)Q.p.B, 0, 0};
+    cuuint64_t gstride[2];
+    cuuint32_t box[3] = {(cuuint32_t)(2 * W), 0, 0}, estr[3] = {1, 1, 1};
+    const int rows = Q.tp.args.rows;
+    if (Q.tp.args.i_dim == 1) {
+      gdim[1] = Q.n;
+      gdim[2] = ringP;
+      gstride[0] = si;
+      gstride[1] = sa;
+      box[1] = rows;
+      box[2] = 1;
+    } else {
+      gdim[1] = ringP;
+      gdim[2] = Q.n;
+      gstride[0] = sa;
+      gstride[1] = si;
+      box[1] = 1;
+      box[2] = rows;
+    }
+    if (enc(&tq.tmap, prec == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, ctx.ring,
+            gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return;
+  }
+  const int64_t tbP = (P.p.B + W - 1) / W, tbQ = (Q.p.B + W - 1) / W;
+  const int64_t tpcP = (int64_t)R * tbP, tpcQ = (int64_t)R * tbQ;
+  unsigned long long* fwd_ctr = ctx.ring_ctr;
+  unsigned long long* back_ctr = ctx.ring_ctr + kRingMaxChunks;
+  Op M = P;
+  M.pipe = true;
+  M.ring_reset = true;
+  M.p.dest[0].ptr = ctx.ring;
+  M.pb = Q.p;
+  M.pb.in = ctx.ring;
+  M.tpb = tq;
+  M.adj_b = Q.adj;
+  PipeArgs& pa = M.ppa;
+  PipeArgs& pq = M.ppb;
+  std::memset(&pa, 0, sizeof(pa));
+  std::memset(&pq, 0, sizeof(pq));
+  pa.tpc = tpcP;
+  pa.npub = 1;
+  pa.pub[0] = fwd_ctr;
+  pa.ring = ringP;
+  pa.ring_role = 1;
+  pa.peer_tpc = tpcQ;
+  pa.peer_ntiles = Q.tp.args.ntiles;
+  pa.back_wait = back_ctr;
+  pa.back_lag = L;
+  pq.tpc = tpcQ;
+  pq.wait = fwd_ctr;
+  pq.ring = ringP;
+  pq.ring_role = 2;
+  pq.ring_discard = (int64_t)W * csize == 128 ? 1 : 0;
+  if (const char* e = getenv("DFFTB_RING_DISCARD")) pq.ring_discard = pq.ring_discard && *e != '0';
+  pq.peer_tpc = tpcP;
+  pq.peer_ntiles = P.tp.args.ntiles;
+  pq.back_pub = back_ctr;
+  for (PipeArgs* x : {&pa, &pq}) {
+    x->timeout_flag = ctx.dstat + 2;
+    x->timeout_ns = 10ull * 1000 * 1000 * 1000;
+  }
+  M.frac = frac;
+  prog[0] = M;
+  prog.erase(prog.begin() + 1);
+}
+
 // One rank's program: fused passes and barriers.  `peer` supplies the
 // exchange-buffer base of any world rank (its own mapping of the peers).
 static std::vector<Op> lower(const Plan& plan, Ctx& ctx, const void* d_in, void* d_out,
                              int parity) {
   std::vector<Op> prog;
-  if (lower_single(plan, ctx, d_in, d_out, parity, prog)) return prog;
+  if (lower_single(plan, ctx, d_in, d_out, parity, prog)) {
+    ring_pairs(prog, ctx);
+    return prog;
+  }
   const int me = ctx.rank;
   const void* cur = d_in;
   bool cur_internal = false;  // d_in has the user layout; exch/work are padded
@@ -1046,6 +1185,7 @@ static std::vector<Op> lower(const Plan& plan, Ctx& ctx, const void* d_in, void*
   }
   fuse_pairs(prog, ctx);
   pipeline_pairs(prog, ctx);
+  ring_pairs(prog, ctx);
   return prog;
 }
 
@@ -1073,7 +1213,23 @@ static void launch_op(const Ctx& ctx, const Op& op, uint64_t epoch, cudaStream_t
     return;
   }
   if (op.pipe) {
+    if (op.ring_reset)
+      CUDA_TRY(cudaMemsetAsync(ctx.ring_ctr, 0, 2 * kRingMaxChunks * sizeof(unsigned long long), s));
     CUDA_TRY(launch_pipe(ctx.prec, op.n, op.p, op.adj, op.tp, op.ppa, op.pb, op.adj_b, op.tpb, op.ppb, op.frac, s));
+    const char* dbg = getenv("DFFTB_RING_DEBUG");
+    if (op.ring_reset && dbg && *dbg == '1') {
+      std::vector<unsigned long long> h(2 * kRingMaxChunks);
+      CUDA_TRY(cudaMemcpyAsync(h.data(), ctx.ring_ctr, h.size() * 8, cudaMemcpyDeviceToHost, s));
+      CUDA_TRY(cudaStreamSynchronize(s));
+      const int C = (int)((op.tp.args.ntiles + op.ppa.tpc - 1) / op.ppa.tpc);
+      fprintf(stderr, "[ring] tpcP %lld ntP %lld tpcQ %lld ntQ %lld chunks %d ring %d lag %d frac %.2f\n",
+              (long long)op.ppa.tpc, (long long)op.tp.args.ntiles, (long long)op.ppb.tpc,
+              (long long)op.tpb.args.ntiles, C, op.ppa.ring, op.ppa.back_lag, op.frac);
+      for (int c = 0; c < C; ++c)
+        if (c < 6 || c > C - 3 || h[c] != (unsigned long long)op.ppa.tpc ||
+            h[kRingMaxChunks + c] != (unsigned long long)op.ppb.tpc)
+          fprintf(stderr, "[ring] chunk %d produced %llu consumed %llu\n", c, h[c], h[kRingMaxChunks + c]);
+    }
     return;
   }
   if (op.generic) CUDA_TRY(launch_generic(ctx.prec, op.g, s));

@@ -47,6 +47,15 @@ struct PipeArgs {
   unsigned long long target[kMaxChunks];
   unsigned long long* timeout_flag;
   unsigned long long timeout_ns;
+  // L2 ring (single GPU, two local passes): the intermediate lives in a ring
+  // of `ring` planes that stays in L2 instead of a full buffer in HBM
+  int ring;          // > 0: planes in the ring (the alpha index wraps)
+  int ring_role;     // 1: producer stores into the ring; 2: consumer loads from it
+  int ring_discard;  // consumer: drop each loaded 128-byte ring row from L2 (no write-back)
+  int64_t peer_tpc, peer_ntiles;  // the other role's tiling: uniform per-chunk targets
+  const unsigned long long* back_wait;  // producer: consumer's per-chunk consumed tiles
+  unsigned long long* back_pub;         // consumer: publishes them
+  int back_lag;                         // chunks the ring holds
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -213,9 +222,31 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
   return t;
 }
 
+// spin until ctr[c] >= tgt (timeout -> flag, carry on)
+__device__ __forceinline__ void spin_ge(const PipeArgs& pp, const unsigned long long* ctr, int c,
+                                        unsigned long long tgt) {
+  // after one timeout the execute is already failed: do not wait again
+  if (ld_acquire_sys_u64(ctr + c) < tgt && ld_acquire_sys_u64(pp.timeout_flag) == 0) {
+    const unsigned long long t0 = globaltimer_ns();
+    while (ld_acquire_sys_u64(ctr + c) < tgt) {
+      if (globaltimer_ns() - t0 > pp.timeout_ns) {
+        atomicExch(pp.timeout_flag, 1ull);
+        break;
+      }
+      __nanosleep(64);
+    }
+  }
+}
+
+// tiles of chunk c for a pass with `tpc` tiles per chunk and `ntiles` in all
+__device__ __forceinline__ unsigned long long chunk_tiles(int64_t tpc, int64_t ntiles, int c) {
+  const int64_t r = ntiles - (int64_t)c * tpc;
+  return (unsigned long long)(r < tpc ? r : tpc);
+}
+
 // consumer side: spin until counter >= target (timeout -> flag, carry on)
 __device__ __forceinline__ void pipe_wait(const PipeArgs& pp, int c) {
-  const unsigned long long tgt = pp.target[c];
+  const unsigned long long tgt = pp.ring ? chunk_tiles(pp.peer_tpc, pp.peer_ntiles, c) : pp.target[c];
   // after one timeout the execute is already failed: do not wait again
   if (ld_acquire_sys_u64(pp.wait + c) < tgt && ld_acquire_sys_u64(pp.timeout_flag) == 0) {
     const unsigned long long t0 = globaltimer_ns();
@@ -255,6 +286,9 @@ __device__ __forceinline__ void pass_tiles(const PassParams& p, const CUtensorMa
   const C* tw = reinterpret_cast<const C*>(p.tw);
   constexpr int ESIZE = LK == kR2C ? (int)sizeof(T) : (int)sizeof(C);
   const T sc = static_cast<T>(p.scale);
+  TwBase<T, N, EPREF> twb;  // per-thread twiddle bases, loaded once
+  load_twbase<T, N, EPREF>(twb, tw, j);
+  const TwBase<T, N, EPREF>* twbp = &twb;
 
   auto decode = [&](int64_t t, int& alpha, int& beta0) {
     int64_t bc;
@@ -299,6 +333,13 @@ __device__ __forceinline__ void pass_tiles(const PassParams& p, const CUtensorMa
     }
     if (tid != 0) return;
     if (PIPE && pp.wait) pipe_wait(pp, (int)(t / pp.tpc));
+    if (PIPE && pp.back_wait) {
+      // ring producer: the slot of chunk c is free once the consumer has
+      // loaded every tile of chunk c - lag
+      const int c = (int)(t / pp.tpc) - pp.back_lag;
+      if (c >= 0) spin_ge(pp, pp.back_wait, c, chunk_tiles(pp.peer_tpc, pp.peer_ntiles, c));
+    }
+    if (PIPE && pp.ring_role == 2) alpha %= pp.ring;
     if constexpr (ADJ) {
       mbar_expect_tx(&bars[s], (uint32_t)(W * N * sizeof(C)));
       for (int r0 = 0; r0 < N; r0 += ta.rows) {
@@ -329,12 +370,23 @@ __device__ __forceinline__ void pass_tiles(const PassParams& p, const CUtensorMa
 
   T lmax = T(0), limag = T(0);  // C2R statistics, reduced once per CTA at the end
   unsigned long long done = 0;  // producer: tiles stored in the current chunk
+  unsigned long long used = 0;  // ring consumer: tiles loaded in the current chunk
   int k = 0;
   for (int64_t t = cta; t < ta.ntiles; t += ncta, ++k) {
     const int s = k % STAGES;
     mbar_wait(&bars[s], (uint32_t)((k / STAGES) & 1));
     int alpha, beta;
     decode(t, alpha, beta);
+    if (PIPE && pp.ring_role == 2 && pp.ring_discard) {
+      // the ring rows of this tile are in shared memory now and no other
+      // tile reads them: drop them from L2 so they are never written back
+      const int aw = alpha % pp.ring;
+      for (int i = tid; i < N; i += W * TPL) {
+        const C* row = reinterpret_cast<const C*>(p.in) + (int64_t)aw * p.in_sa + (int64_t)beta * p.in_sb +
+                       (int64_t)i * p.in_si;
+        asm volatile("discard.global.L2 [%0], 128;" ::"l"(row) : "memory");
+      }
+    }
     beta += w;
     const unsigned char* st = stg + s * TL::STG;
     C v[SC::E];
@@ -374,20 +426,30 @@ __device__ __forceinline__ void pass_tiles(const PassParams& p, const CUtensorMa
 #if DFFTB_EXP_NOCOMPUTE  // timing experiment only (wrong results): data movement alone
     (void)tw;
 #else
-    run_stages<T, N, EPREF, 0>(v, xch + w * LS, tw, j);
+    run_stages<T, N, EPREF, 0>(v, xch + w * LS, tw, j, twbp);
 #endif
-#if DFFTB_EXP_NOSTORE  // timing experiment only: compute without the global stores
-    if (p.scale == 12345.0 && beta < p.B) store_lk<T, N, EPREF, LK>(p, sptr, v, j, alpha, beta, sc);
-#else
-    if (beta < p.B) store_lk<T, N, EPREF, LK, SPEC>(p, sptr, v, j, alpha, beta, sc);
-#endif
+    const int alpha_st = (PIPE && pp.ring_role == 1) ? alpha % pp.ring : alpha;
+    if (beta < p.B) store_lk<T, N, EPREF, LK, SPEC>(p, sptr, v, j, alpha_st, beta, sc);
+    if (PIPE && pp.back_pub) {
+      // ring consumer: this tile's ring rows were loaded (and discarded)
+      ++used;
+      const int64_t c = t / pp.tpc;
+      if (t + ncta >= ta.ntiles || (t + ncta) / pp.tpc != c) {
+        __syncthreads();
+        if (tid == 0)
+          asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(pp.back_pub + c), "l"(used) : "memory");
+        used = 0;
+      }
+    }
     if (PIPE && pp.npub) {
       // producer: publish a chunk once this CTA has no further tile in it
       ++done;
       const int64_t c = t / pp.tpc;
       if (t + ncta >= ta.ntiles || (t + ncta) / pp.tpc != c) {
+        // gpu scope: bar.sync orders the CTA's stores before thread 0's
+        // red.release (cumulativity, the CUTLASS semaphore pattern); peers on
+        // other GPUs get a full system fence from every thread
         if (pp.pub_sys) __threadfence_system();
-        else __threadfence();
         __syncthreads();
         if (tid == 0) {
           for (int q = 0; q < pp.npub; ++q) {

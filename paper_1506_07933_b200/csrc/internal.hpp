@@ -143,6 +143,10 @@ struct Ctx {
   // pipelined pass pairs: cumulative per-chunk counter targets of each
   // counter slot (identical on every rank: all ranks run the same programs)
   std::vector<std::array<unsigned long long, 32>> pipe_cum;
+  // single-GPU L2 plane ring of the fused rows->columns pass pair
+  void* ring = nullptr;
+  size_t ring_bytes = 0;
+  unsigned long long* ring_ctr = nullptr;  // [2 * kRingMaxChunks]: produced, consumed
   bool c2r_pending = false;
 
   void* exch(int rank, int slot, int parity) const;

@@ -23,6 +23,7 @@ import paper_1506_07933_b200 as D  # noqa: E402
 from gpu_util import make_plan, rel_l2  # noqa: E402
 
 TOL = {"f64": 1e-12, "f32": 1e-5}
+FLAG_DEV = "cpu" if os.environ.get("DFFTB_TEST_OVERSUBSCRIBE") == "1" else "cuda"  # gloo vs nccl
 
 
 def cases(P):
@@ -75,8 +76,15 @@ def main():
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
+    if os.environ.get("DFFTB_TEST_OVERSUBSCRIBE") == "1":
+        # more ranks than GPUs (e.g. 8 ranks on 4 GPUs): exercises the 8-rank
+        # process / IPC / group logic; two contexts share each GPU by time slicing
+        local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if os.environ.get("DFFTB_TEST_OVERSUBSCRIBE") == "1":
+        dist.init_process_group("gloo")  # NCCL refuses two ranks on one GPU
+    else:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     ok = True
     for decomp, dims, grid, kind, prec in cases(world):
         fwd = make_plan(decomp, dims, grid, kind, "forward", prec)
@@ -111,7 +119,7 @@ def main():
         ctx.check()
         del os.environ["DFFTB_PIPE"]
         pipe_ok = bool(torch.equal(yp.data, y.data)) and bool(torch.equal(zp.data, z.data))
-        flags = torch.tensor([1 if spec_ok else 0, 1 if pipe_ok else 0], device="cuda")
+        flags = torch.tensor([1 if spec_ok else 0, 1 if pipe_ok else 0], device=FLAG_DEV)
         dist.all_reduce(flags, op=dist.ReduceOp.MIN)
         if rank == 0:
             good = bool(flags[0].item() == 1 and flags[1].item() == 1)
@@ -120,7 +128,7 @@ def main():
                   f"pipelined pairs bit-identical {bool(flags[1].item())}", flush=True)
         ctx.close()
         dist.barrier()
-    flag = torch.tensor([1 if ok else 0], device="cuda")
+    flag = torch.tensor([1 if ok else 0], device=FLAG_DEV)
     dist.broadcast(flag, 0)
     dist.destroy_process_group()
     sys.exit(0 if flag.item() == 1 else 1)

@@ -40,6 +40,7 @@ static constexpr size_t kFlagsBytes = 4096;
 static constexpr unsigned long long kBarrierTimeoutNs = 60ull * 1000 * 1000 * 1000;
 
 void* Ctx::exch(int r, int slot, int parity) const {
+  if (slot < 0 || slot >= exch_slots) raise(DFFTB_ArenaExhausted, "exchange slot out of range");
   char* base = static_cast<char*>(peer_region[r]);
   return base + flags_bytes + (size_t)(2 * slot + parity) * exch_bytes;
 }
@@ -95,6 +96,23 @@ static size_t family_bytes(const Plan& plan) {
     }
   }
   return (size_t)m * 2 * plan.prec;
+}
+
+// Exchange slots a program of the plan family uses: one per transpose stage
+// (pencil 2, slab 1, 4-D general 3), at least the 2 the single-rank
+// backward lowering uses.
+static int family_exch_slots(const Plan& plan) {
+  dfftb_plan_options o = plan.options;
+  const int kf = plan.kind == DFFTB_C2C ? DFFTB_C2C : DFFTB_R2C;
+  const int kb = plan.kind == DFFTB_C2C ? DFFTB_C2C : DFFTB_C2R;
+  int m = 2;
+  for (int d = 0; d < 2; ++d) {
+    Plan p = build_plan(plan.dims, plan.decomp, plan.grid, d == 0 ? kf : kb, d, plan.prec, o);
+    int t = 0;
+    for (const auto& st : p.stages) t += st.type == StageType::Transpose;
+    m = std::max(m, t);
+  }
+  return m;
 }
 
 static bool is_pow2(int64_t n) { return n >= 1 && (n & (n - 1)) == 0; }
@@ -211,7 +229,8 @@ Ctx* ctx_create(const Plan& plan, int rank, int device) {
   const size_t blk = (family_bytes(plan) + 255) / 256 * 256;
   ctx->flags_bytes = kFlagsBytes;
   ctx->exch_bytes = blk;
-  ctx->region_bytes = kFlagsBytes + 4 * blk;
+  ctx->exch_slots = family_exch_slots(plan);
+  ctx->region_bytes = kFlagsBytes + 2 * (size_t)ctx->exch_slots * blk;  // [slot][parity] buffers
   ctx->work_bytes = blk;
   CUDA_TRY(cudaMalloc(&ctx->region, ctx->region_bytes));
   CUDA_TRY(cudaMemset(ctx->region, 0, kFlagsBytes));

@@ -146,6 +146,7 @@ struct Ctx {
   // single-GPU L2 plane ring of the fused rows->columns pass pair
   void* ring = nullptr;
   size_t ring_bytes = 0;
+  int exch_slots = 2;  // exchange buffers per parity in the shared region
   unsigned long long* ring_ctr = nullptr;  // [2 * kRingMaxChunks]: produced, consumed
   bool c2r_pending = false;
 

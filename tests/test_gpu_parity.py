@@ -294,3 +294,25 @@ def test_config_B_256_r2c_against_oracle():
     fwd = make_plan("slab", dims, [1], "r2c", "forward")
     y = run_world(fwd, xg)
     assert rel_l2(y, y_ref) <= 1e-12
+
+
+def test_general_4d_repeated_executes_stay_exact():
+    # a 4-D general plan has three transposes -> three exchange slots per
+    # execute parity; repeated executes (both parities) must agree bitwise
+    # with the first and with the oracle (regression: the third slot once
+    # ran past the shared region on odd executes)
+    dims = [8, 8, 16, 16]
+    fwd = make_plan("general", dims, [1, 1, 1], "c2c", "forward")
+    bwd = make_plan("general", dims, [1, 1, 1], "c2c", "backward")
+    ctx = D.make_context(fwd)
+    x = D.DistTensor.seeded(fwd.input, 0)
+    y0 = D.execute(fwd, x, ctx).data.clone()
+    for _ in range(4):
+        y = D.execute(fwd, x, ctx)
+        z = D.execute(bwd, y, ctx)
+        ctx.check()
+        assert torch.equal(y.data, y0)
+        assert rel_l2(z.data.cpu().numpy(), x.data.cpu().numpy()) < 1e-14
+    xg = O.seeded(dims, True, "f64")
+    y_ref, _ = O.execute(xg, dims, "general", [1, 1, 1], "c2c", "forward", "f64")
+    assert rel_l2(y0.cpu().numpy().reshape(dims), y_ref) <= 1e-12

@@ -14,6 +14,8 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cmath>
 #include <complex>
 #include <cstdint>
 #include <cstring>
@@ -428,6 +430,142 @@ inline GlobalDims hat_dims(const GlobalDims& dims, TransformKind kind) {
   GlobalDims out = dims;
   if (kind == TransformKind::R2C && !out.extent.empty()) out.extent.back() = out.extent.back() / 2 + 1;
   return out;
+}
+
+// ------------------------------------------------- spectral (spectral.hpp)
+struct WavenumberMap {  // spectral.hpp:17-20
+  std::vector<std::vector<double>> axis_k;
+  std::vector<std::vector<double>> axis_k_deriv;
+};
+
+/// wavenumbers (spectral.hpp:24-56) for this rank's block of a forward plan's
+/// output layout (`freq` must be such a layout: NotFrequencyLayout otherwise).
+inline WavenumberMap wavenumbers(const Distribution& freq, const GlobalDims& spatial_dims,
+                                 std::span<const double> domain_lengths, int rank) {
+  (void)spatial_dims;  // the plan handle behind `freq` carries the spatial dims
+  if (domain_lengths.size() != freq.dims.ndim())
+    throw Error(ErrorCode::NotFrequencyLayout, "NotFrequencyLayout: one domain length per axis");
+  const LocalExtents ext = freq.extents_of(rank);
+  WavenumberMap m;
+  for (std::size_t a = 0; a < freq.dims.ndim(); ++a) {
+    for (int deriv = 0; deriv < 2; ++deriv) {
+      std::vector<double> k(static_cast<std::size_t>(std::max<std::int64_t>(1, ext.axes[a].length)));
+      check(dfftb_wavenumbers(freq.plan->h, rank, static_cast<int>(a), deriv, domain_lengths.data(), k.data()));
+      k.resize(static_cast<std::size_t>(ext.axes[a].length));
+      (deriv ? m.axis_k_deriv : m.axis_k).push_back(std::move(k));
+    }
+  }
+  return m;
+}
+
+template <class T>
+struct SpectralContext {  // spectral.hpp:61-70
+  Comm* comm = nullptr;
+  GlobalDims dims;
+  ProcessGrid grid;
+  std::vector<double> domain_lengths;
+  Plan<T> fwd_c2c, bwd_c2c, fwd_r2c, bwd_c2r;
+  WavenumberMap k_c2c, k_r2c;
+  ExecContext exec;
+};
+
+/// make_spectral_context (spectral.hpp:72-98): the four plans on one grid
+/// (pencil for 3 axes on a 2-D grid, the general decomposition otherwise),
+/// their wavenumbers and one shared execution context.
+template <class T>
+SpectralContext<T> make_spectral_context(Comm& comm, const GlobalDims& dims, const ProcessGrid& grid,
+                                         std::vector<double> domain_lengths = {}) {
+  SpectralContext<T> c;
+  c.comm = &comm;
+  c.dims = dims;
+  c.grid = grid;
+  if (domain_lengths.empty()) domain_lengths.assign(dims.ndim(), 6.283185307179586476925);
+  c.domain_lengths = std::move(domain_lengths);
+  auto mk = [&](TransformKind k, Direction d) {
+    return (dims.ndim() == 3 && grid.ndim() == 2) ? plan_pencil<T>(dims, grid, k, d)
+                                                  : plan_general<T>(dims, grid, k, d);
+  };
+  c.fwd_c2c = mk(TransformKind::C2C, Direction::Forward);
+  c.bwd_c2c = mk(TransformKind::C2C, Direction::Backward);
+  c.fwd_r2c = mk(TransformKind::R2C, Direction::Forward);
+  c.bwd_c2r = mk(TransformKind::C2R, Direction::Backward);
+  c.k_c2c = wavenumbers(c.fwd_c2c.output, dims, c.domain_lengths, comm.rank());
+  c.k_r2c = wavenumbers(c.fwd_r2c.output, dims, c.domain_lengths, comm.rank());
+  c.exec = make_context(c.fwd_c2c, comm);
+  return c;
+}
+
+namespace detail {
+/// op (spectral multiplier) fused into the forward transform's last pass
+/// (dfftb_execute_spectral); accumulate adds into `spec`.
+template <class T>
+void forward_op(SpectralContext<T>& c, const Plan<T>& fwd, const DistTensor<T>& x, int op, int axis,
+                DistTensor<T>& spec, bool accumulate) {
+  if (!(x.dist == fwd.input))
+    throw Error(ErrorCode::LayoutMismatch, "LayoutMismatch: input layout differs from the plan's");
+  check(dfftb_execute_spectral(fwd.handle->h, c.exec.ctx->h, x.d_data(), spec.d_data(), op, axis,
+                               c.domain_lengths.data(), accumulate ? 1 : 0, c.exec.stream, DFFTB_EXEC_SYNC));
+}
+template <class T>
+bool is_real_field(const DistTensor<T>& x) {
+  return x.dist.element == ElementKind::Real;
+}
+}  // namespace detail
+
+/// derivative (spectral.hpp:131-164): backward(i k_axis (.) forward(x)), normalized
+template <class T>
+DistTensor<T> derivative(SpectralContext<T>& c, const DistTensor<T>& x, int axis) {
+  const bool real = detail::is_real_field(x);
+  const Plan<T>& fwd = real ? c.fwd_r2c : c.fwd_c2c;
+  const Plan<T>& bwd = real ? c.bwd_c2r : c.bwd_c2c;
+  auto spec = DistTensor<T>::zeros(fwd.output, x.rank);
+  detail::forward_op(c, fwd, x, DFFTB_SPECTRAL_DERIV, axis, spec, false);
+  return execute(bwd, spec, c.exec);
+}
+
+/// gradient (spectral.hpp:167-176)
+template <class T>
+std::vector<DistTensor<T>> gradient(SpectralContext<T>& c, const DistTensor<T>& x) {
+  std::vector<DistTensor<T>> g;
+  for (std::size_t a = 0; a < c.dims.ndim(); ++a) g.push_back(derivative(c, x, static_cast<int>(a)));
+  return g;
+}
+
+/// divergence (spectral.hpp:180-216): sum_j i k_j (.) forward(c_j), one inverse
+template <class T>
+DistTensor<T> divergence(SpectralContext<T>& c, const std::vector<DistTensor<T>>& comps) {
+  if (comps.size() != c.dims.ndim())
+    throw Error(ErrorCode::GridMismatch, "GridMismatch: one component per axis required");
+  const bool real = detail::is_real_field(comps[0]);
+  const Plan<T>& fwd = real ? c.fwd_r2c : c.fwd_c2c;
+  const Plan<T>& bwd = real ? c.bwd_c2r : c.bwd_c2c;
+  auto acc = DistTensor<T>::zeros(fwd.output, comps[0].rank);
+  for (std::size_t a = 0; a < comps.size(); ++a)
+    detail::forward_op(c, fwd, comps[a], DFFTB_SPECTRAL_DERIV, static_cast<int>(a), acc, a > 0);
+  return execute(bwd, acc, c.exec);
+}
+
+/// laplacian (spectral.hpp:219-249): backward(-|k|^2 (.) forward(x))
+template <class T>
+DistTensor<T> laplacian(SpectralContext<T>& c, const DistTensor<T>& x) {
+  const bool real = detail::is_real_field(x);
+  const Plan<T>& fwd = real ? c.fwd_r2c : c.fwd_c2c;
+  const Plan<T>& bwd = real ? c.bwd_c2r : c.bwd_c2c;
+  auto spec = DistTensor<T>::zeros(fwd.output, x.rank);
+  detail::forward_op(c, fwd, x, DFFTB_SPECTRAL_LAPLACIAN, 0, spec, false);
+  return execute(bwd, spec, c.exec);
+}
+
+/// inverse_laplacian (spectral.hpp:251-309): divides by -|k|^2, k = 0 pinned
+/// to zero; NonZeroMean unless the field has zero mean
+template <class T>
+DistTensor<T> inverse_laplacian(SpectralContext<T>& c, const DistTensor<T>& x) {
+  const bool real = detail::is_real_field(x);
+  const Plan<T>& fwd = real ? c.fwd_r2c : c.fwd_c2c;
+  const Plan<T>& bwd = real ? c.bwd_c2r : c.bwd_c2c;
+  auto spec = DistTensor<T>::zeros(fwd.output, x.rank);
+  detail::forward_op(c, fwd, x, DFFTB_SPECTRAL_INV_LAPLACIAN, 0, spec, false);
+  return execute(bwd, spec, c.exec);
 }
 
 }  // namespace dfftb::dfft

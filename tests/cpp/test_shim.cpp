@@ -2,6 +2,7 @@
 // test_layout.cpp) compiled against the dfftb C++ shim (include/dfftb/dfft.hpp)
 // instead of the reference headers.  `--host` runs only the plan/layout
 // checks (no GPU needed); without it the single-rank execute checks run too.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -177,11 +178,66 @@ static void gpu_tests() {
   }
 }
 
+// spectral.hpp mirror (test_spectral.cpp:79-100, 274-292): d/dz sin(2z) =
+// 2 cos(2z) for real and complex fields; div(grad f) == lap f; inverse
+// Laplacian round trip; NonZeroMean
+static void spectral_tests() {
+  LocalComm comm;
+  const GlobalDims dims{8, 8, 16};
+  auto c = make_spectral_context<double>(comm, dims, ProcessGrid{1, 1});
+  CHECK(c.k_c2c.axis_k[0].size() == 8 && c.k_r2c.axis_k[2].size() == 9);
+  CHECK(c.k_c2c.axis_k_deriv[2][8] == 0.0);  // Nyquist zeroed for derivatives
+  const double tp = 2.0 * M_PI;
+  auto field = [&](auto fn, bool real) {
+    auto x = DistTensor<double>::zeros(real ? c.fwd_r2c.input : c.fwd_c2c.input, 0);
+    fill_from_global(x, [&](std::int64_t, std::span<const std::int64_t> g) {
+      const double z = tp * g[0] / 8, y = tp * g[1] / 8, w = tp * g[2] / 16;
+      return cxd(fn(z, y, w), 0.0);
+    });
+    return x;
+  };
+  for (bool real : {true, false}) {
+    auto x = field([](double, double, double w) { return std::sin(2 * w); }, real);
+    auto g = gradient(c, x);
+    g[2].to_host();
+    double err = 0;
+    for (int i = 0; i < 8 * 8 * 16; ++i) {
+      const double w = tp * (i % 16) / 16;
+      const double got = real ? g[2].real[i] : g[2].cplx[i].real();
+      err = std::max(err, std::fabs(got - 2 * std::cos(2 * w)));
+    }
+    CHECK(err < 1e-10);
+  }
+  auto f = field([](double z, double y, double w) { return std::sin(3 * z) * std::cos(2 * y) + std::sin(5 * w); },
+                 true);
+  auto dg = divergence(c, gradient(c, f));
+  auto lp = laplacian(c, f);
+  dg.to_host();
+  lp.to_host();
+  double e = 0, m = 0;
+  for (std::size_t i = 0; i < lp.real.size(); ++i) {
+    e = std::max(e, std::fabs(dg.real[i] - lp.real[i]));
+    m = std::max(m, std::fabs(lp.real[i]));
+  }
+  CHECK(e < 1e-9 * m);
+  auto u = inverse_laplacian(c, lp);  // zero-mean field: recovers f
+  u.to_host();
+  f.to_host();
+  double eu = 0;
+  for (std::size_t i = 0; i < f.real.size(); ++i) eu = std::max(eu, std::fabs(u.real[i] - f.real[i]));
+  CHECK(eu < 1e-10);
+  auto ones = field([](double, double, double) { return 1.0; }, true);
+  CHECK_THROWS_WITH(inverse_laplacian(c, ones), "NonZeroMean");
+}
+
 int main(int argc, char** argv) {
   const bool host_only = argc > 1 && std::strcmp(argv[1], "--host") == 0;
   try {
     host_tests();
-    if (!host_only) gpu_tests();
+    if (!host_only) {
+      gpu_tests();
+      spectral_tests();
+    }
   } catch (const std::exception& e) {
     std::printf("uncaught: %s\n", e.what());
     ++g_fail;

@@ -6,9 +6,11 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <fstream>
 #include <string>
 
 #include "dfftb/dfft.hpp"
+#include "dfftb/tensor_file.hpp"
 
 using namespace dfftb::dfft;
 using cxd = cx<double>;
@@ -230,11 +232,46 @@ static void spectral_tests() {
   CHECK_THROWS_WITH(inverse_laplacian(c, ones), "NonZeroMean");
 }
 
+// tensor_file.hpp mirror: DTNS write/read round trip through a layout, the
+// file format (golden header bytes) and the error codes
+static void tensor_file_tests() {
+  LocalComm comm;
+  auto plan = plan_pencil<double>(GlobalDims{4, 3, 5}, ProcessGrid{1, 1}, TransformKind::R2C, Direction::Forward);
+  auto x = DistTensor<double>::zeros(plan.input, 0);
+  fill_from_global(x, [](std::int64_t flat, std::span<const std::int64_t>) { return cxd(0.5 * flat - 3.0, 0); });
+  const std::string path = "/tmp/dfftb_shim_tensor.dtns";
+  write_tensor(comm, x, path);
+  const TensorFile f = read_tensor_file(path);
+  CHECK(f.dims == (GlobalDims{4, 3, 5}) && f.element == TensorElement::Real64 && f.payload.size() == 60 * 8);
+  auto y = read_tensor<double>(comm, plan.input, path);
+  y.to_host();
+  bool same = y.real.size() == 60;
+  for (int i = 0; same && i < 60; ++i) same = y.real[i] == 0.5 * i - 3.0;
+  CHECK(same);
+  // a real file feeding a complex layout is promoted
+  auto c2c = plan_pencil<double>(GlobalDims{4, 3, 5}, ProcessGrid{1, 1}, TransformKind::C2C, Direction::Forward);
+  auto z = read_tensor<double>(comm, c2c.input, path);
+  z.to_host();
+  CHECK(z.cplx.size() == 60 && z.cplx[7] == cxd(0.5, 0.0));
+  // header layout: "DTNS", u32 1, u8 kind, u32 axes, u64 dims
+  std::ifstream in(path, std::ios::binary);
+  unsigned char h[13];
+  in.read(reinterpret_cast<char*>(h), 13);
+  CHECK(std::memcmp(h, "DTNS", 4) == 0 && h[4] == 1 && h[8] == 0 && h[9] == 3);
+  auto other = plan_pencil<double>(GlobalDims{4, 3, 6}, ProcessGrid{1, 1}, TransformKind::C2C, Direction::Forward);
+  CHECK_THROWS_WITH(read_tensor<double>(comm, other.input, path), "DimMismatch");
+  std::ofstream(path, std::ios::binary) << "NOPE....";
+  CHECK_THROWS_WITH(read_tensor_file(path), "TruncatedFile");
+  std::ofstream(path, std::ios::binary) << "NOPE0000000000000";
+  CHECK_THROWS_WITH(read_tensor_file(path), "BadMagic");
+}
+
 int main(int argc, char** argv) {
   const bool host_only = argc > 1 && std::strcmp(argv[1], "--host") == 0;
   try {
     host_tests();
     if (!host_only) {
+      tensor_file_tests();
       gpu_tests();
       spectral_tests();
     }

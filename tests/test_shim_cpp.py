@@ -15,6 +15,7 @@ def _build():
     src = os.path.join(HERE, "cpp", "test_shim.cpp")
     if os.path.exists(BIN) and os.path.getmtime(BIN) > max(
             os.path.getmtime(src), os.path.getmtime(os.path.join(ROOT, "include", "dfftb", "dfft.hpp")),
+            os.path.getmtime(os.path.join(ROOT, "include", "dfftb", "tensor_file.hpp")),
             os.path.getmtime(os.path.join(PKG, "libdfftb.so"))):
         return
     cmd = ["g++", "-std=c++20", "-O1", "-o", BIN, src, "-I", os.path.join(ROOT, "include"),

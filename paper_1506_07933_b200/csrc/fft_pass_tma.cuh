@@ -409,8 +409,8 @@ __device__ __forceinline__ void pass_tiles(const PassParams& p, const CUtensorMa
         const C* scp = reinterpret_cast<const C*>(st) + w * ll;
         for (int i = j; i <= N / 2; i += TPL) {  // stored bins only, not the row padding
           const C x = scp[i];
-          const T m = sqrt(x.x * x.x + x.y * x.y);
-          lmax = m > lmax ? m : lmax;
+          const T m2 = x.x * x.x + x.y * x.y;  // max |X|^2, one sqrt per CTA (monotone: exact)
+          lmax = m2 > lmax ? m2 : lmax;
           if (i == 0 || i == N / 2) limag = fabs(x.y) > limag ? fabs(x.y) : limag;
         }
       }
@@ -463,7 +463,7 @@ __device__ __forceinline__ void pass_tiles(const PassParams& p, const CUtensorMa
       }
     }
   }
-  if constexpr (LK == kC2R) herm_reduce<T>(p.herm, lmax, limag);
+  if constexpr (LK == kC2R) herm_reduce<T>(p.herm, sqrt(lmax), limag);
 }
 
 // The single-pass kernel.  Its body is the tile loop of pass_tiles written
@@ -580,8 +580,8 @@ __global__ void __launch_bounds__(W* Sched<N, EPREF>::TPL, DFFTB_TMA_MINB)
         const C* scp = reinterpret_cast<const C*>(st) + w * ll;
         for (int i = j; i <= N / 2; i += TPL) {  // stored bins only, not the row padding
           const C x = scp[i];
-          const T m = sqrt(x.x * x.x + x.y * x.y);
-          lmax = m > lmax ? m : lmax;
+          const T m2 = x.x * x.x + x.y * x.y;  // max |X|^2, one sqrt per CTA (monotone: exact)
+          lmax = m2 > lmax ? m2 : lmax;
           if (i == 0 || i == N / 2) limag = fabs(x.y) > limag ? fabs(x.y) : limag;
         }
       }
@@ -597,7 +597,7 @@ __global__ void __launch_bounds__(W* Sched<N, EPREF>::TPL, DFFTB_TMA_MINB)
     run_stages<T, N, EPREF, 0>(v, lane, tw, j, twbp);
     if (beta < p.B) store_lk<T, N, EPREF, LK, SPEC>(p, sptr, v, j, alpha, beta, sc);
   }
-  if constexpr (LK == kC2R) herm_reduce<T>(p.herm, lmax, limag);
+  if constexpr (LK == kC2R) herm_reduce<T>(p.herm, sqrt(lmax), limag);
 }
 
 // Pipelined pair: CTAs [0, ncta_a) run the producer pass, the rest the

@@ -110,7 +110,8 @@ struct TmaLayout {
 
 // stage-0 fetch from a staging slot, compile-time lane kind
 template <typename T, int N, int EPREF, int LK, class LDC, class LDR>
-__device__ __forceinline__ void fetch0_lk(Cpx<T>* v, int j, LDC ldc, LDR ldr) {
+__device__ __forceinline__ void fetch0_lk(Cpx<T>* v, int j, LDC ldc, LDR ldr, T* m2 = nullptr,
+                                          T* mi = nullptr) {
   using C = Cpx<T>;
   using SC = Sched<N, EPREF>;
   constexpr int E = SC::E;
@@ -136,6 +137,14 @@ __device__ __forceinline__ void fetch0_lk(Cpx<T>* v, int j, LDC ldc, LDR ldr) {
         // statistics are taken from the staged bins by the kernel.)
         const bool lo = pos <= N / 2;
         x = ldc(lo ? pos : N - pos);
+        if (m2) {
+          // NonHermitian statistics of the stored bins as they are read
+          // (every bin 0..N/2 is read at least once; max is idempotent):
+          // block max |X|^2 and the DC / Nyquist imaginary residues
+          const T a = x.x * x.x + x.y * x.y;
+          *m2 = a > *m2 ? a : *m2;
+          if (pos == 0 || pos == N / 2) *mi = fabs(x.y) > *mi ? fabs(x.y) : *mi;
+        }
         if (pos == 0 || pos == N / 2) x.y = T(0);
         if (lo) x.y = -x.y;
       }
@@ -398,22 +407,12 @@ __device__ __forceinline__ void pass_tiles(const PassParams& p, const CUtensorMa
       const int ll = ta.lane_bytes / ESIZE;  // stored lane length in elements
       const C* scp = reinterpret_cast<const C*>(st) + w * ll;
       const T* srp = reinterpret_cast<const T*>(st) + w * ll;
+      // C2R: NonHermitian statistics (max |X|^2 -> one sqrt per CTA, exact by
+      // monotonicity; DC / Nyquist |Im|) of active lanes, taken in the fetch
+      const bool stats = LK == kC2R && beta < p.B;
       fetch0_lk<T, N, EPREF, LK>(
-          v, j, [&](int pos) { return scp[pos]; }, [&](int pos) { return srp[pos]; });
-    }
-    if constexpr (LK == kC2R) {
-      // NonHermitian statistics straight from the staged half spectrum:
-      // block max |X| and the DC / Nyquist imaginary residues of active lanes
-      if (beta < p.B) {
-        const int ll = ta.lane_bytes / ESIZE;
-        const C* scp = reinterpret_cast<const C*>(st) + w * ll;
-        for (int i = j; i <= N / 2; i += TPL) {  // stored bins only, not the row padding
-          const C x = scp[i];
-          const T m2 = x.x * x.x + x.y * x.y;  // max |X|^2, one sqrt per CTA (monotone: exact)
-          lmax = m2 > lmax ? m2 : lmax;
-          if (i == 0 || i == N / 2) limag = fabs(x.y) > limag ? fabs(x.y) : limag;
-        }
-      }
+          v, j, [&](int pos) { return scp[pos]; }, [&](int pos) { return srp[pos]; },
+          stats ? &lmax : nullptr, stats ? &limag : nullptr);
     }
     __syncthreads();  // staging slot s fully consumed by every thread
     {
@@ -569,22 +568,12 @@ __global__ void __launch_bounds__(W* Sched<N, EPREF>::TPL, DFFTB_TMA_MINB)
       const int ll = ta.lane_bytes / ESIZE;  // stored lane length in elements
       const C* scp = reinterpret_cast<const C*>(st) + w * ll;
       const T* srp = reinterpret_cast<const T*>(st) + w * ll;
+      // C2R: NonHermitian statistics (max |X|^2 -> one sqrt per CTA, exact by
+      // monotonicity; DC / Nyquist |Im|) of active lanes, taken in the fetch
+      const bool stats = LK == kC2R && beta < p.B;
       fetch0_lk<T, N, EPREF, LK>(
-          v, j, [&](int pos) { return scp[pos]; }, [&](int pos) { return srp[pos]; });
-    }
-    if constexpr (LK == kC2R) {
-      // NonHermitian statistics straight from the staged half spectrum:
-      // block max |X| and the DC / Nyquist imaginary residues of active lanes
-      if (beta < p.B) {
-        const int ll = ta.lane_bytes / ESIZE;
-        const C* scp = reinterpret_cast<const C*>(st) + w * ll;
-        for (int i = j; i <= N / 2; i += TPL) {  // stored bins only, not the row padding
-          const C x = scp[i];
-          const T m2 = x.x * x.x + x.y * x.y;  // max |X|^2, one sqrt per CTA (monotone: exact)
-          lmax = m2 > lmax ? m2 : lmax;
-          if (i == 0 || i == N / 2) limag = fabs(x.y) > limag ? fabs(x.y) : limag;
-        }
-      }
+          v, j, [&](int pos) { return scp[pos]; }, [&](int pos) { return srp[pos]; },
+          stats ? &lmax : nullptr, stats ? &limag : nullptr);
     }
     __syncthreads();  // staging slot s fully consumed by every thread
     {

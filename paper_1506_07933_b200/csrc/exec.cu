@@ -505,7 +505,17 @@ static bool plan_tma(Op& op, int prec) {
     if (p.A1 > 1) return false;  // 4-D strided lanes: direct kernel (3-D tensor map only)
     if ((2 * W * prec) % 16 != 0 || 2 * W > 256) return false;
     const int64_t si = p.in_si * csize, sa = (p.A > 1 ? p.in_sa : (int64_t)n * p.in_si) * csize;
-    if (si % 16 || sa % 16 || (p.in_sb != 1)) return false;
+    if (p.in_sb != 1) return false;
+    if (si % 16 || sa % 16) {
+      // rows a tensor map cannot describe (fp32 C2R user blocks: 129-bin
+      // rows of 1032 bytes): per-thread 8-byte cp.async into the same tile
+      if (csize != 8 || (reinterpret_cast<uintptr_t>(p.in) & 7)) return false;
+      const char* e = getenv("DFFTB_UNALIGNED_LDGSTS");
+      if (e && *e == '0') return false;
+      tp.args.bulk = 0;
+      tp.args.ldgsts = 1;
+      return true;
+    }
     tp.args.bulk = 0;
     {
       // row loader: TMA boxes (default; measured faster even for 4-16 MB row

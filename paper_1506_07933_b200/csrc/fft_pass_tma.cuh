@@ -333,9 +333,14 @@ __device__ __forceinline__ void pass_tiles(const PassParams& p, const CUtensorMa
         const int i = e / W, ww = e - (e / W) * W;
         const bool ok = beta0 + ww < p.B;
         const C* src = src0 + (int64_t)(ok ? beta0 + ww : 0) * p.in_sb + (int64_t)i * p.in_si;
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst + (size_t)e * sizeof(C))),
-                     "l"(src), "r"(ok ? 16 : 0)
-                     : "memory");
+        if constexpr (sizeof(C) == 16)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst + (size_t)e * sizeof(C))),
+                       "l"(src), "r"(ok ? 16 : 0)
+                       : "memory");
+        else  // fp32 complex: 8-byte copies (rows only 8-byte aligned)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst + (size_t)e * sizeof(C))),
+                       "l"(src), "r"(ok ? 8 : 0)
+                       : "memory");
       }
       asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&bars[s])) : "memory");
       return;
@@ -515,9 +520,14 @@ __global__ void __launch_bounds__(W* Sched<N, EPREF>::TPL, DFFTB_TMA_MINB)
         const int i = e / W, ww = e - (e / W) * W;
         const bool ok = beta0 + ww < p.B;
         const C* src = src0 + (int64_t)(ok ? beta0 + ww : 0) * p.in_sb + (int64_t)i * p.in_si;
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst + (size_t)e * sizeof(C))),
-                     "l"(src), "r"(ok ? 16 : 0)
-                     : "memory");
+        if constexpr (sizeof(C) == 16)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst + (size_t)e * sizeof(C))),
+                       "l"(src), "r"(ok ? 16 : 0)
+                       : "memory");
+        else  // fp32 complex: 8-byte copies (rows only 8-byte aligned)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst + (size_t)e * sizeof(C))),
+                       "l"(src), "r"(ok ? 8 : 0)
+                       : "memory");
       }
       asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&bars[s])) : "memory");
       return;

@@ -137,6 +137,13 @@ dfftb_status dfftb_plan_exchange_counts(dfftb_plan plan, int rank, int transpose
                                         int64_t* send_counts, int64_t* recv_counts,
                                         int* group_size);
 
+/* Device bytes dfftb_ctx_create allocates for this plan's family on rank
+ * `rank` (the symmetric exchange region: flag page + one buffer per
+ * transpose stage and execute parity, plus the private work buffer); the
+ * reference sizes its StagingArena in make_context (plan.hpp:365-390,
+ * exchange.hpp:250-262).  Host-only: no CUDA call. */
+dfftb_status dfftb_workspace_bytes(dfftb_plan plan, int rank, uint64_t* bytes);
+
 /* ---- execution contexts (make_context, plan.hpp:365-390) ---------------- */
 
 /* Per-rank context on CUDA device `device`: allocates the symmetric exchange

@@ -29,4 +29,5 @@ from .dfft import (  # noqa: F401
     plan_general,
     plan_pencil,
     plan_slab,
+    workspace_bytes,
 )

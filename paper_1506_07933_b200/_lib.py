@@ -64,6 +64,7 @@ _SIGS = {
     "dfftb_kernel_launch_count": (_c.c_uint64, []),
     "dfftb_spectral_apply": (_c.c_int, [vp, _c.c_int, _c.c_int, _c.c_int,
                                         _c.POINTER(_c.c_double), vp, vp, _c.c_int, vp]),
+    "dfftb_workspace_bytes": (_c.c_int, [vp, _c.c_int, _c.POINTER(_c.c_uint64)]),
     "dfftb_execute_spectral": (_c.c_int, [vp, vp, vp, vp, _c.c_int, _c.c_int, _c.POINTER(_c.c_double),
                                           _c.c_int, vp, _c.c_int]),
     "dfftb_wavenumbers": (_c.c_int, [vp, _c.c_int, _c.c_int, _c.c_int,

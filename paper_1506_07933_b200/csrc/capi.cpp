@@ -162,6 +162,10 @@ dfftb_status dfftb_local_index(dfftb_plan plan, int side, const int64_t* coord, 
   });
 }
 
+dfftb_status dfftb_workspace_bytes(dfftb_plan plan, int rank, uint64_t* bytes) {
+  return guarded([&] { *bytes = (uint64_t)dfftb::workspace_bytes(plan->plan, rank); });
+}
+
 dfftb_status dfftb_plan_exchange_counts(dfftb_plan plan, int rank, int transpose_index,
                                         int64_t* send_counts, int64_t* recv_counts,
                                         int* group_size) {

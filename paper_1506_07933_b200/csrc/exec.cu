@@ -212,6 +212,12 @@ static std::pair<void*, void*> bluestein_tables(int64_t n, int prec) {
   return {upload(chirp), upload(b)};
 }
 
+size_t workspace_bytes(const Plan& plan, int rank) {
+  if (rank < 0 || rank >= plan.nranks()) raise(DFFTB_InvalidRank, "rank out of range");
+  const size_t blk = (family_bytes(plan) + 255) / 256 * 256;
+  return kFlagsBytes + 2 * (size_t)family_exch_slots(plan) * blk + blk + 8 * sizeof(unsigned long long);
+}
+
 Ctx* ctx_create(const Plan& plan, int rank, int device) {
   if (rank < 0 || rank >= plan.nranks()) raise(DFFTB_InvalidRank, "rank out of range");
   check_lengths(plan);

@@ -7,6 +7,7 @@
 
 namespace dfftb {
 
+size_t workspace_bytes(const Plan& plan, int rank);
 Ctx* ctx_create(const Plan& plan, int rank, int device);
 void ctx_export(const Ctx& ctx, CtxHandle* h);
 void ctx_connect(Ctx& ctx, const CtxHandle* handles);

@@ -158,6 +158,14 @@ def block_map(n: int, p: int) -> Tuple[List[int], List[int]]:
     return list(c), list(o)
 
 
+def workspace_bytes(plan: "Plan", rank: int) -> int:
+    """Device bytes make_context allocates for `plan`'s family on `rank`
+    (dfftb_workspace_bytes; host-only)."""
+    v = ctypes.c_uint64()
+    _check(_lib.lib().dfftb_workspace_bytes(plan._h, rank, ctypes.byref(v)))
+    return int(v.value)
+
+
 def hat_dims(dims: Sequence[int], kind: TransformKind) -> Tuple[int, ...]:
     """layout.hpp:201-207: R2C stores floor(N_last/2)+1 bins on the last axis."""
     d = list(dims)

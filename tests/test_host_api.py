@@ -185,3 +185,17 @@ def test_gloo_world_size_2_host_path():
     for p in ps:
         p.join(timeout=60)
     assert res == {0: "ok", 1: "ok"}, res
+
+
+def test_workspace_bytes():
+    # dfftb_workspace_bytes (host-only): flag page + one exchange buffer per
+    # transpose stage and parity + the work buffer, each sized for the
+    # largest block of the plan family
+    p = D.plan_pencil((512, 512, 512), (2, 4), D.TransformKind.C2C, D.Direction.Forward)
+    blk = 512 ** 3 * 16 // 8
+    assert D.workspace_bytes(p, 0) == 4096 + 2 * 2 * blk + blk + 64
+    g = D.plan_general((8, 8, 16, 16), (1, 1, 1), D.TransformKind.C2C, D.Direction.Forward)
+    blk = 8 * 8 * 16 * 16 * 16
+    assert D.workspace_bytes(g, 0) == 4096 + 2 * 3 * blk + blk + 64  # three transposes
+    with pytest.raises(D.Error, match="InvalidRank"):
+        D.workspace_bytes(p, 8)

@@ -474,6 +474,19 @@ static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   return fn;
 }
 
+// L2 sector promotion of the strided-lane tensor maps (A/B aid:
+// DFFTB_L2PROMO = 0 none, 1 64 B, 2 128 B, 3 256 B (default))
+static CUtensorMapL2promotion l2_promotion() {
+  const char* e = getenv("DFFTB_L2PROMO");
+  const int v = e ? atoi(e) : 3;
+  switch (v) {
+    case 0: return CU_TENSOR_MAP_L2_PROMOTION_NONE;
+    case 1: return CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
+    case 2: return CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+    default: return CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  }
+}
+
 static bool tma_disabled() {
   static int v = -1;
   if (v < 0) {
@@ -559,7 +572,7 @@ static bool plan_tma(Op& op, int prec) {
     }
     CUresult r = enc(&tp.tmap, prec == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
                      3, const_cast<void*>(p.in), gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                     CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_SWIZZLE_NONE, l2_promotion(),
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return false;
     tp.args.rows = rows;

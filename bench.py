@@ -28,6 +28,8 @@ METRIC = "3D FFT GFLOP/s (5NlogN) & fwd+inv time, 512^3 C2C fp64, 1/2/4/8 B200"
 UNIT = "GFLOP/s"
 FLOP_FWDINV = 2 * 5 * (512 ** 3) * 27  # bench.cpp:32-41, x2 for fwd+inv
 REF_BIN = os.path.join(ROOT, "oracle", "_ref", "dfft_ref")
+NVL_NOMINAL_GBS = 900.0   # NVLink 5, per direction per GPU
+NVL_MEASURED_GBS = 703.0  # SM peer stores, all GPUs at once (tools/p2p_store_probe.cu)
 
 
 def grid_for(n):
@@ -204,6 +206,7 @@ def main():
     import torch.distributed as dist
 
     import paper_1506_07933_b200 as D
+    from paper_1506_07933_b200.telemetry import NvlinkCounters
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -252,7 +255,9 @@ def main():
     sampler = ClockSampler(local) if rank == 0 else None
     if sampler:
         sampler.start()
+    nvl = NvlinkCounters(local) if world > 1 else None
     barrier()
+    nvl0 = nvl.read() if nvl and nvl.available else None
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     l_before = D.kernel_launch_count()
@@ -263,12 +268,35 @@ def main():
     e1.record(stream)
     barrier()
     t_host1 = time.time()
+    nvl1 = nvl.read() if nvl0 else None
     l_timed = D.kernel_launch_count() - l_before
     if sampler:
         sampler.stop()
         sampler.window = (t_host0, t_host1)
     ms = max_over_ranks(e0.elapsed_time(e1)) / K
     ctx.check()
+    nvl_meas = None
+    if world > 1:
+        # driver NVLink data counters around the timed region (NVML), per GPU
+        ok = 1.0 if nvl1 else 0.0
+        tx = (nvl1[0] - nvl0[0]) / K if nvl1 else 0.0
+        rx = (nvl1[1] - nvl0[1]) / K if nvl1 else 0.0
+        t = torch.tensor([ok, tx, rx, tx, rx], dtype=torch.float64, device=dev)
+        tmin = t.clone()
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(tmin, op=dist.ReduceOp.MIN)
+        if tmin[0].item() == 1.0:
+            n_loc_max = max(fwd.input.local_count(r) for r in range(world))
+            p0_, p1_ = grid
+            expect = 2 * 16 * n_loc_max * ((p1_ - 1) / p1_ + (p0_ - 1) / p0_)
+            nvl_meas = {"source": "NVML NVLINK_THROUGHPUT_DATA_TX/RX (driver counters, all links)",
+                        "tx_bytes_per_step_per_gpu_max": t[1].item(),
+                        "rx_bytes_per_step_per_gpu_max": t[2].item(),
+                        "tx_bytes_per_step_per_gpu_min": tmin[3].item(),
+                        "algorithmic_bytes_per_step_per_gpu": expect,
+                        "tx_GBs_over_step": t[1].item() / (ms * 1e-3) / 1e9}
+        else:
+            nvl_meas = {"unavailable": nvl.why if nvl and not nvl.available else "counter read failed"}
 
     # parity of what was timed: round trip of the last step
     rt = (torch.linalg.vector_norm(z.data - x.data) ** 2).item()
@@ -370,7 +398,9 @@ def main():
         t_hbm = 2 * 6 * 16 * n_loc / (peak * 1e9)
         p0, p1 = grid
         nvl = 2 * 16 * n_loc * ((p1 - 1) / p1 + (p0 - 1) / p0)
-        t_nvl = nvl / 770e9
+        # measured NVLink figure: SM-issued peer stores, all GPUs at once
+        # (tools/p2p_store_probe.cu, profiles/r2_p2p_probe.txt); nominal below
+        t_nvl = nvl / (NVL_MEASURED_GBS * 1e9)
         # SURVEY §8(d) convention: nominal 8 TB/s HBM and 900 GB/s NVLink
         t_nominal = max(2 * 6 * 16 * n_loc / 8.0e12, nvl / 900e9)
         traffic = None
@@ -401,9 +431,12 @@ def main():
                          "step_bound": "nvlink" if t_nvl > t_hbm else "hbm",
                          "step_roofline_ms": 1e3 * max(t_hbm, t_nvl),
                          "step_frac": 1e3 * max(t_hbm, t_nvl) / ms,
+                         "nvlink_peak_measured_GBs": NVL_MEASURED_GBS,
+                         "nvlink_peak_nominal_GBs": NVL_NOMINAL_GBS,
                          "step_roofline_ms_nominal_8TBs_900GBs": 1e3 * t_nominal,
                          "step_frac_nominal": 1e3 * t_nominal / ms},
             "clocks": sampler.summary() if sampler else None,
+            "nvlink_counters": nvl_meas,
             "e2e": e2e,
             "cpu_baseline": cpu,
             "fwd_breakdown_ms": {"local_fft": tb_f.local_fft / 3 * 1e3,

@@ -177,6 +177,14 @@ dfftb_status dfftb_ctx_check(dfftb_ctx ctx, void* stream);
  * logic when fewer GPUs than ranks exist): creates P connected contexts on
  * one device, and runs all ranks' stages in lockstep on one stream. */
 dfftb_status dfftb_world_create(dfftb_plan plan, int device, dfftb_ctx* ctxs);
+/* The same world over several devices of this process: rank r's context on
+ * devices[r % ndevices].  Exchange stores cross NVLink through direct peer
+ * pointers; dfftb_execute_world orders the ranks' passes with cross-device
+ * CUDA events issued by the host (no kernel waits on another), on the
+ * contexts' own streams, and makes `stream` (on ctxs[0]'s device) wait for
+ * all of them. */
+dfftb_status dfftb_world_create_devices(dfftb_plan plan, int ndevices, const int* devices,
+                                        dfftb_ctx* ctxs);
 dfftb_status dfftb_execute_world(dfftb_plan plan, dfftb_ctx* ctxs,
                                  const void* const* d_in, void* const* d_out,
                                  void* stream, int flags);
@@ -193,6 +201,13 @@ dfftb_status dfftb_fill_seeded(dfftb_plan plan, int rank, int side, uint64_t see
  * this thread, formatted like dfft::Error::what(): "<CodeName>: <what>". */
 const char* dfftb_error_name(dfftb_status status);
 const char* dfftb_last_error_message(void);
+
+/* Per-op device times of the last execute that was given `timers`, in
+ * program order: kinds[i] 0 = local FFT pass, 1 = exchange pass (FFT whose
+ * stores go to other ranks' buffers), 2 = sync point; streams[i] 1 = the
+ * overlapped pass on the context's side stream; lengths[i] = the transform
+ * length.  Returns the op count (arrays filled up to `max`). */
+int dfftb_ctx_last_ops(dfftb_ctx ctx, int* kinds, int* streams, int* lengths, double* ms, int max);
 
 /* Number of dfftb kernels launched by this process so far (evidence counter). */
 uint64_t dfftb_kernel_launch_count(void);
@@ -223,6 +238,11 @@ dfftb_status dfftb_spectral_apply(dfftb_plan forward_plan, int rank, int op, int
 dfftb_status dfftb_execute_spectral(dfftb_plan forward_plan, dfftb_ctx ctx, const void* d_in, void* d_out,
                                     int op, int axis, const double* domain_lengths, int accumulate,
                                     void* stream, int flags);
+/* dfftb_execute_spectral for every rank of an emulated world
+ * (dfftb_world_create / _devices), in lockstep like dfftb_execute_world. */
+dfftb_status dfftb_execute_world_spectral(dfftb_plan forward_plan, dfftb_ctx* ctxs, const void* const* d_in,
+                                          void* const* d_out, int op, int axis, const double* domain_lengths,
+                                          int accumulate, void* stream, int flags);
 /* wavenumbers (spectral.hpp:24-56): the local k values of `axis` for this
  * rank's frequency block (length = local extent); deriv != 0 gives
  * axis_k_deriv (Nyquist zeroed), else axis_k. */

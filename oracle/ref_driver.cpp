@@ -20,7 +20,7 @@
 // Usage:
 //   dfft_ref --dims 64,64,64 --decomp slab|pencil --grid 1|2,4
 //            --kind c2c|r2c --prec f64|f32 [--seed 1] [--warmup 1] [--reps 3]
-//            [--dump PREFIX] [--no-normalize]
+//            [--dump PREFIX] [--no-normalize] [--spectral]
 // Prints one JSON line.  With --dump writes PREFIX.in.bin (global input, real
 // for r2c / interleaved complex for c2c), PREFIX.fwd.bin (global forward
 // spectrum, interleaved complex, frequency layout gathered in xyz order) and
@@ -37,6 +37,7 @@
 #include <vector>
 
 #include "dfft/plan.hpp"
+#include "dfft/spectral.hpp"
 
 using namespace dfft;
 
@@ -74,6 +75,7 @@ struct Args {
   int warmup = 1;
   int reps = 3;
   bool normalize = true;
+  bool spectral = false;
   std::string dump;
 };
 
@@ -250,6 +252,67 @@ int run(const Args& a) {
   return 0;
 }
 
+// --spectral: the reference's spectral operators (spectral.hpp:131-309) on
+// the seeded field through make_spectral_context (pencil / general plans over
+// --grid): PREFIX.in.bin, PREFIX.d<a>.bin (derivative along axis a),
+// PREFIX.lap.bin (laplacian), PREFIX.ilap.bin (inverse_laplacian of the
+// laplacian: a zero-mean input), PREFIX.div.bin (divergence of the gradient),
+// all global arrays in the input's element kind.
+template <class T>
+int run_spectral(const Args& a) {
+  int P = 1;
+  for (auto g : a.grid) P *= static_cast<int>(g);
+  std::vector<std::vector<T>> out_real;
+  std::vector<std::vector<cx<T>>> out_cplx;
+  std::vector<std::string> names;
+  transport::spawn_world(P, [&](transport::Comm& comm) {
+    std::vector<int> g(a.grid.begin(), a.grid.end());
+    auto sc = make_spectral_context<T>(comm, GlobalDims(a.dims), ProcessGrid(g));
+    const auto& in_dist = a.r2c ? sc.fwd_r2c.input : sc.fwd_c2c.input;
+    auto x = DistTensor<T>::zeros(in_dist, comm.rank());
+    fill_from_global(x, [&](std::int64_t flat, std::span<const std::int64_t>) {
+      const double re = unit_from_hash(a.seed * 0x10001 + 2 * flat);
+      const double im = a.r2c ? 0.0 : unit_from_hash(a.seed * 0x10001 + 2 * flat + 1);
+      return cx<T>(static_cast<T>(re), static_cast<T>(im));
+    });
+    std::vector<std::pair<std::string, DistTensor<T>>> res;
+    res.emplace_back("in", x);
+    std::vector<DistTensor<T>> grad;
+    for (std::size_t ax = 0; ax < a.dims.size(); ++ax) {
+      grad.push_back(derivative(sc, x, static_cast<int>(ax)));
+      res.emplace_back("d" + std::to_string(ax), grad.back());
+    }
+    auto lap = laplacian(sc, x);
+    res.emplace_back("lap", lap);
+    // fp32: the laplacian's mean is zero only to fp32 rounding, above the
+    // reference's 1e-12 N zero-mean bound (NonZeroMean): no ilap golden
+    if constexpr (std::is_same_v<T, double>) res.emplace_back("ilap", inverse_laplacian(sc, lap));
+    res.emplace_back("div", divergence(sc, grad));
+    for (auto& [name, t] : res) {
+      if (a.r2c) {
+        auto gl = gather_global_real(comm, t);
+        if (comm.rank() == 0) {
+          names.push_back(name);
+          out_real.push_back(std::move(gl));
+        }
+      } else {
+        auto gl = gather_global_complex(comm, t);
+        if (comm.rank() == 0) {
+          names.push_back(name);
+          out_cplx.push_back(std::move(gl));
+        }
+      }
+    }
+  });
+  for (std::size_t i = 0; i < names.size(); ++i) {
+    const std::string path = a.dump + "." + names[i] + ".bin";
+    if (a.r2c) write_file(path, out_real[i].data(), out_real[i].size() * sizeof(T));
+    else write_file(path, out_cplx[i].data(), out_cplx[i].size() * sizeof(cx<T>));
+  }
+  std::printf("{\"impl\":\"reference\",\"spectral\":%zu}\n", names.size());
+  return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -277,12 +340,14 @@ int main(int argc, char** argv) {
     else if (k == "--reps") a.reps = std::atoi(next());
     else if (k == "--dump") a.dump = next();
     else if (k == "--no-normalize") a.normalize = false;
+    else if (k == "--spectral") a.spectral = true;
     else {
       std::fprintf(stderr, "unknown flag %s\n", k.c_str());
       return 2;
     }
   }
   try {
+    if (a.spectral) return a.f32 ? run_spectral<float>(a) : run_spectral<double>(a);
     return a.f32 ? run<float>(a) : run<double>(a);
   } catch (const std::exception& e) {
     std::printf("{\"impl\":\"reference\",\"error\":\"%s\"}\n", e.what());

@@ -234,12 +234,21 @@ dfftb_status dfftb_ctx_check(dfftb_ctx ctx, void* stream) {
 }
 
 dfftb_status dfftb_world_create(dfftb_plan plan, int device, dfftb_ctx* ctxs) {
+  return dfftb_world_create_devices(plan, 1, &device, ctxs);
+}
+
+dfftb_status dfftb_world_create_devices(dfftb_plan plan, int ndevices, const int* devices, dfftb_ctx* ctxs) {
   return guarded([&] {
+    if (!devices || ndevices < 1) dfftb::raise(DFFTB_ConfigInvalid, "need at least one device");
     const int P = plan->plan.nranks();
     std::vector<dfftb::Ctx*> raw(P, nullptr);
-    dfftb::world_create(plan->plan, device, raw.data());
+    dfftb::world_create(plan->plan, devices, ndevices, raw.data());
     for (int r = 0; r < P; ++r) ctxs[r] = new dfftb_ctx_s{raw[r]};
   });
+}
+
+int dfftb_ctx_last_ops(dfftb_ctx ctx, int* kinds, int* streams, int* lengths, double* ms, int max) {
+  return ctx ? dfftb::last_op_times(*ctx->ctx, kinds, streams, lengths, ms, max) : 0;
 }
 
 dfftb_status dfftb_execute_world(dfftb_plan plan, dfftb_ctx* ctxs, const void* const* d_in,
@@ -284,6 +293,18 @@ dfftb_status dfftb_execute_spectral(dfftb_plan forward_plan, dfftb_ctx ctx, cons
   return guarded([&] {
     dfftb::execute_spectral(forward_plan->plan, *ctx->ctx, d_in, d_out, op, axis, domain_lengths, accumulate,
                             static_cast<cudaStream_t>(stream), flags);
+  });
+}
+
+dfftb_status dfftb_execute_world_spectral(dfftb_plan forward_plan, dfftb_ctx* ctxs, const void* const* d_in,
+                                          void* const* d_out, int op, int axis, const double* domain_lengths,
+                                          int accumulate, void* stream, int flags) {
+  return guarded([&] {
+    const int P = forward_plan->plan.nranks();
+    std::vector<dfftb::Ctx*> raw(P);
+    for (int r = 0; r < P; ++r) raw[r] = ctxs[r]->ctx;
+    dfftb::execute_world_spectral(forward_plan->plan, raw.data(), d_in, d_out, op, axis, domain_lengths, accumulate,
+                                  static_cast<cudaStream_t>(stream), flags);
   });
 }
 

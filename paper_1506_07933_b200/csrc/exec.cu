@@ -1,5 +1,6 @@
 // dfftb executor: contexts (make_context, plan.hpp:359-390), lowering of a
-// plan to fused GPU passes + group barriers, and execute (plan.hpp:463-535).
+// plan to fused GPU passes + cross-GPU sync points, and execute
+// (plan.hpp:463-535).
 //
 // Lowering.  The reference runs, per rank, LocalFftStage -> TransposeStage
 // (pack, all_to_all, unpack; exchange.hpp:547-590) [-> LocalTransposeStage]
@@ -7,20 +8,34 @@
 // whose store epilogue writes each output element to its final address in
 // the stage's target layout:
 //   FFT followed by a transpose  -> peer exchange buffers of the grid-axis
-//                                   group (NVLink stores), then a barrier
+//                                   group (NVLink stores), then a sync point
 //   FFT followed by Normalize    -> user output, scaled by 1/N
 //   last FFT                     -> user output
 //   FFT followed by a local FFT  -> private work buffer
 // so each axis costs one read + one write of the local block.
+//
+// Overlap (pipelined_all_to_all, exchange.hpp:323-423).  An
+// exchange pass followed by a local pass is split into chunks along the lane
+// axis both passes share: the exchange pass runs chunk after chunk on the
+// caller's stream and signals each finished chunk to its group; the local
+// pass runs on a side stream, on the other SMs, and starts chunk c as soon as
+// every group member has signalled it -- the NVLink-bound pass and the
+// HBM-bound pass run concurrently instead of back to back.
+//
+// Programs are lowered once per (plan, buffers, parity) and cached in the
+// context; the launches of a cached program are captured into a CUDA graph.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include <unistd.h>
 
 #include <algorithm>
 #include <complex>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
+#include <string>
 #include <vector>
 
 #include "exec.hpp"
@@ -35,9 +50,50 @@ namespace dfftb {
       raise(DFFTB_CudaError, std::string(#x) + ": " + cudaGetErrorString(e_));    \
   } while (0)
 
-static constexpr uint64_t kHandleMagic = 0x64666674625f3031ull;  // "dfftb_01"
-static constexpr size_t kFlagsBytes = 4096;
-static constexpr unsigned long long kBarrierTimeoutNs = 60ull * 1000 * 1000 * 1000;
+static constexpr uint64_t kHandleMagic = 0x64666674625f3032ull;  // "dfftb_02"
+static constexpr size_t kFlagsBytes = (size_t)kSyncSlots * kMaxRanksDev * sizeof(unsigned long long);
+static constexpr unsigned long long kSyncTimeoutNs = 60ull * 1000 * 1000 * 1000;
+static constexpr int kStatEpoch = 6;
+static constexpr int kStatWords = 8;
+static constexpr size_t kMaxCachedPrograms = 64;
+
+// ------------------------------------------------------------------- knobs
+// Read once per process (never on the execute path).  Defaults are the
+// shipped configuration; the variables exist for A/B measurements.
+struct Knobs {
+  bool zperm = true;          // DFFTB_ZPERM: axis-0 pass input stored [x1][x0][rest]
+  bool single_reorder = true; // DFFTB_SINGLE_REORDER: 1-rank backward in forward axis order
+  bool tma = true;            // DFFTB_NO_TMA=1 disables the TMA pass kernel
+  int l2promo = 3;            // DFFTB_L2PROMO: tensor-map L2 promotion 0/64/128/256 B
+  bool unaligned_ldgsts = true;  // DFFTB_UNALIGNED_LDGSTS: cp.async loader for odd fp32 rows
+  bool overlap = true;        // DFFTB_OVERLAP: pipelined exchange/local pass pairs
+  int chunks = 4;             // DFFTB_OVERLAP_CHUNKS: chunks per pipelined pair
+  double frac = -1.0;         // DFFTB_OVERLAP_FRAC: SM share of the exchange pass (<0: model)
+  bool graphs = true;         // DFFTB_GRAPHS: replay cached programs as CUDA graphs
+  bool op_times = false;      // DFFTB_OP_TIMES: print per-op device times of timed executes
+};
+
+static const Knobs& knobs() {
+  static const Knobs k = [] {
+    Knobs k;
+    auto flag = [](const char* name, bool def) {
+      const char* e = getenv(name);
+      return e && *e ? *e != '0' : def;
+    };
+    k.zperm = flag("DFFTB_ZPERM", true);
+    k.single_reorder = flag("DFFTB_SINGLE_REORDER", true);
+    k.tma = !flag("DFFTB_NO_TMA", false);
+    if (const char* e = getenv("DFFTB_L2PROMO")) k.l2promo = atoi(e);
+    k.unaligned_ldgsts = flag("DFFTB_UNALIGNED_LDGSTS", true);
+    k.overlap = flag("DFFTB_OVERLAP", true);
+    if (const char* e = getenv("DFFTB_OVERLAP_CHUNKS")) k.chunks = std::max(1, std::min(16, atoi(e)));
+    if (const char* e = getenv("DFFTB_OVERLAP_FRAC")) k.frac = atof(e);
+    k.graphs = flag("DFFTB_GRAPHS", true);
+    k.op_times = flag("DFFTB_OP_TIMES", false);
+    return k;
+  }();
+  return k;
+}
 
 void* Ctx::exch(int r, int slot, int parity) const {
   if (slot < 0 || slot >= exch_slots) raise(DFFTB_ArenaExhausted, "exchange slot out of range");
@@ -58,6 +114,11 @@ struct DeviceGuard {
     cudaGetDevice(&cur);
     if (prev >= 0 && cur != prev) cudaSetDevice(prev);
   }
+};
+
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
 };
 
 // Internal (exchange / work) buffers keep the reference's axis order but pad
@@ -159,6 +220,7 @@ static void check_lengths(const Plan& plan) {
   }
   for (int g : plan.grid)
     if (g > kMaxDest) raise(DFFTB_Unsupported, "grid factors above 8 are not supported");
+  if (plan.nranks() > kMaxRanksDev) raise(DFFTB_Unsupported, "at most 64 ranks");
 }
 
 // host FFT (recursive radix-2, double) for the Bluestein kernel spectrum
@@ -179,6 +241,23 @@ static void host_fft(std::vector<std::complex<double>>& a) {
   }
 }
 
+static void* upload_complex(const std::vector<std::complex<double>>& v, int prec) {
+  void* d = nullptr;
+  if (prec == 8) {
+    CUDA_TRY(cudaMalloc(&d, v.size() * 16));
+    CUDA_TRY(cudaMemcpy(d, v.data(), v.size() * 16, cudaMemcpyHostToDevice));
+  } else {
+    std::vector<float> f(2 * v.size());
+    for (size_t i = 0; i < v.size(); ++i) {
+      f[2 * i] = (float)v[i].real();
+      f[2 * i + 1] = (float)v[i].imag();
+    }
+    CUDA_TRY(cudaMalloc(&d, f.size() * 4));
+    CUDA_TRY(cudaMemcpy(d, f.data(), f.size() * 4, cudaMemcpyHostToDevice));
+  }
+  return d;
+}
+
 // Bluestein tables for the forward direction (bluestein_context,
 // kernels.hpp:179-216): chirp c_j = exp(-i pi (j^2 mod 2n) / n) and the
 // kernel spectrum FFT_m(wrapped conj(c)) / m, in double, cast to T
@@ -193,29 +272,27 @@ static std::pair<void*, void*> bluestein_tables(int64_t n, int prec) {
   for (int64_t j = 1; j < n; ++j) b[j] = b[m - j] = std::conj(chirp[j]);
   host_fft(b);
   for (auto& v : b) v /= (double)m;
-  auto upload = [&](const std::vector<std::complex<double>>& v) {
-    void* d = nullptr;
-    if (prec == 8) {
-      CUDA_TRY(cudaMalloc(&d, v.size() * 16));
-      CUDA_TRY(cudaMemcpy(d, v.data(), v.size() * 16, cudaMemcpyHostToDevice));
-    } else {
-      std::vector<float> f(2 * v.size());
-      for (size_t i = 0; i < v.size(); ++i) {
-        f[2 * i] = (float)v[i].real();
-        f[2 * i + 1] = (float)v[i].imag();
-      }
-      CUDA_TRY(cudaMalloc(&d, f.size() * 4));
-      CUDA_TRY(cudaMemcpy(d, f.data(), f.size() * 4, cudaMemcpyHostToDevice));
-    }
-    return d;
-  };
-  return {upload(chirp), upload(b)};
+  return {upload_complex(chirp, prec), upload_complex(b, prec)};
+}
+
+// device bytes of the per-axis tables ctx_create uploads
+static size_t table_bytes(const Plan& plan) {
+  size_t t = 0;
+  std::vector<int64_t> seen;
+  for (auto n : plan.dims) {
+    if (std::find(seen.begin(), seen.end(), n) != seen.end()) continue;
+    seen.push_back(n);
+    if (is_pow2(n)) t += (size_t)n * 2 * plan.prec;
+    else if (!is_smooth(n)) t += (size_t)(n + bluestein_m(n)) * 2 * plan.prec;
+  }
+  return t;
 }
 
 size_t workspace_bytes(const Plan& plan, int rank) {
   if (rank < 0 || rank >= plan.nranks()) raise(DFFTB_InvalidRank, "rank out of range");
   const size_t blk = (family_bytes(plan) + 255) / 256 * 256;
-  return kFlagsBytes + 2 * (size_t)family_exch_slots(plan) * blk + blk + 8 * sizeof(unsigned long long);
+  return kFlagsBytes + 2 * (size_t)family_exch_slots(plan) * blk + blk + kStatWords * sizeof(unsigned long long) +
+         table_bytes(plan);
 }
 
 Ctx* ctx_create(const Plan& plan, int rank, int device) {
@@ -238,60 +315,30 @@ Ctx* ctx_create(const Plan& plan, int rank, int device) {
   ctx->exch_slots = family_exch_slots(plan);
   ctx->region_bytes = kFlagsBytes + 2 * (size_t)ctx->exch_slots * blk;  // [slot][parity] buffers
   ctx->work_bytes = blk;
+  ctx->table_bytes = table_bytes(plan);
   CUDA_TRY(cudaMalloc(&ctx->region, ctx->region_bytes));
   CUDA_TRY(cudaMemset(ctx->region, 0, kFlagsBytes));
   CUDA_TRY(cudaMalloc(&ctx->work, ctx->work_bytes));
-  CUDA_TRY(cudaMalloc(&ctx->dstat, 8 * sizeof(unsigned long long)));
-  CUDA_TRY(cudaMemset(ctx->dstat, 0, 8 * sizeof(unsigned long long)));
+  CUDA_TRY(cudaMalloc(&ctx->dstat, kStatWords * sizeof(unsigned long long)));
+  CUDA_TRY(cudaMemset(ctx->dstat, 0, kStatWords * sizeof(unsigned long long)));
   // twiddle tables w[m] = exp(-2 pi i m / n) in double, cast to T
   // (TwiddleTable, kernels.hpp:66-98); forward only: backward is conj(F(conj x))
   for (auto n64 : plan.dims) {
     const int n = (int)n64;
     if (!is_pow2(n) && !is_smooth(n) && !ctx->bluestein.count(n)) ctx->bluestein[n] = bluestein_tables(n, plan.prec);
     if (!is_pow2(n) || ctx->twiddles.count(n)) continue;
-    std::vector<double> wd(2 * n);
-    std::vector<float> wf(2 * n);
+    std::vector<std::complex<double>> w(n);
     for (int m = 0; m < n; ++m) {
       const double a = -2.0 * M_PI * (double)m / (double)n;
-      wd[2 * m] = std::cos(a);
-      wd[2 * m + 1] = std::sin(a);
-      wf[2 * m] = (float)wd[2 * m];
-      wf[2 * m + 1] = (float)wd[2 * m + 1];
+      w[m] = {std::cos(a), std::sin(a)};
     }
-    void* d = nullptr;
-    CUDA_TRY(cudaMalloc(&d, 2 * n * plan.prec));
-    CUDA_TRY(cudaMemcpy(d, plan.prec == 8 ? (void*)wd.data() : (void*)wf.data(), 2 * n * plan.prec,
-                        cudaMemcpyHostToDevice));
-    ctx->twiddles[n] = d;
+    ctx->twiddles[n] = upload_complex(w, plan.prec);
   }
-  // L2-resident plane ring for the fused two-axis pass (slab plans and
-  // pencil grids whose second grid factor is 1: the row exchange is local)
-  {
-    // experimental, opt-in (DFFTB_FUSE=1): measured 5.8 ms vs 4.76 ms for the
-    // two plain passes at 512^3 (round 1) -- the pipeline is latency-bound
-    const char* on = getenv("DFFTB_FUSE");
-    const bool fusable_grid = plan.decomp == DFFTB_SLAB || (plan.grid.size() == 2 && plan.grid[1] == 1);
-    if ((on && *on == '1') && fusable_grid && plan.dims.size() == 3 && plan.dims[1] == plan.dims[2] &&
-        fused2_supported(plan.prec, (int)plan.dims[1])) {
-      const char* le = getenv("DFFTB_FUSE_L");
-      const int L = le ? std::max(2, atoi(le)) : 8;
-      ctx->fuse_planes = (int)plan.dims[0];
-      ctx->fuse_ring_bytes = (size_t)L * plan.dims[1] * plan.dims[2] * 2 * plan.prec;
-      CUDA_TRY(cudaMalloc(&ctx->fuse_ring, ctx->fuse_ring_bytes));
-      CUDA_TRY(cudaMalloc(&ctx->fuse_counters, 2 * sizeof(unsigned int) * ctx->fuse_planes));
-      // reserve persisting L2 for the ring so its dirty lines are overwritten
-      // in L2 instead of being written back (DFFTB_FUSE_PERSIST=0 disables)
-      const char* pe = getenv("DFFTB_FUSE_PERSIST");
-      if (!(pe && *pe == '0')) {
-        int maxp = 0;
-        cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, device);
-        const size_t want = std::min<size_t>((size_t)maxp, ctx->fuse_ring_bytes);
-        if (want > 0 && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) == cudaSuccess)
-          ctx->fuse_persist_bytes = want;
-        cudaGetLastError();
-      }
-    }
-  }
+  cudaStream_t side = nullptr, cap = nullptr;
+  CUDA_TRY(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+  CUDA_TRY(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+  ctx->side = side;
+  ctx->capture = cap;
   ctx->peer_region.assign(ctx->nranks, nullptr);
   ctx->peer_opened.assign(ctx->nranks, false);
   ctx->peer_region[rank] = ctx->region;
@@ -312,6 +359,17 @@ void ctx_export(const Ctx& ctx, CtxHandle* h) {
   h->magic = kHandleMagic;
 }
 
+static void enable_peer(int dev, int peer) {
+  if (dev == peer) return;
+  int can = 0;
+  CUDA_TRY(cudaDeviceCanAccessPeer(&can, dev, peer));
+  if (!can) raise(DFFTB_Unsupported, "no peer access between devices");
+  DeviceGuard g(dev);
+  cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+  if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) raise(DFFTB_CudaError, cudaGetErrorString(e));
+  cudaGetLastError();
+}
+
 void ctx_connect(Ctx& ctx, const CtxHandle* handles) {
   DeviceGuard g(ctx.device);
   for (int r = 0; r < ctx.nranks; ++r) {
@@ -321,15 +379,7 @@ void ctx_connect(Ctx& ctx, const CtxHandle* handles) {
     if (r == ctx.rank) continue;
     if (h.pid == (int64_t)getpid()) {
       // same process (thread-per-GPU world): direct peer pointer
-      if (h.device != ctx.device) {
-        int can = 0;
-        CUDA_TRY(cudaDeviceCanAccessPeer(&can, ctx.device, (int)h.device));
-        if (!can) raise(DFFTB_Unsupported, "no peer access between devices");
-        cudaError_t e = cudaDeviceEnablePeerAccess((int)h.device, 0);
-        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
-          raise(DFFTB_CudaError, cudaGetErrorString(e));
-        cudaGetLastError();
-      }
+      enable_peer(ctx.device, (int)h.device);
       ctx.peer_region[r] = (void*)(uintptr_t)h.dptr;
     } else {
       cudaIpcMemHandle_t ih;
@@ -343,11 +393,14 @@ void ctx_connect(Ctx& ctx, const CtxHandle* handles) {
   ctx.connected = true;
 }
 
+static void drop_programs(Ctx& ctx);
+
 void ctx_destroy(Ctx* ctx) {
   if (!ctx) return;
   {
     DeviceGuard g(ctx->device);
     cudaDeviceSynchronize();
+    drop_programs(*ctx);
     for (int r = 0; r < ctx->nranks; ++r)
       if (ctx->peer_opened[r]) cudaIpcCloseMemHandle(ctx->peer_region[r]);
     for (auto& kv : ctx->twiddles) cudaFree(kv.second);
@@ -355,23 +408,31 @@ void ctx_destroy(Ctx* ctx) {
       cudaFree(kv.second.first);
       cudaFree(kv.second.second);
     }
+    for (void* e : ctx->events) cudaEventDestroy(static_cast<cudaEvent_t>(e));
+    if (ctx->side) cudaStreamDestroy(static_cast<cudaStream_t>(ctx->side));
+    if (ctx->capture) cudaStreamDestroy(static_cast<cudaStream_t>(ctx->capture));
     cudaFree(ctx->region);
     cudaFree(ctx->work);
     cudaFree(ctx->dstat);
-    if (ctx->fuse_ring) cudaFree(ctx->fuse_ring);
-    if (ctx->ring) cudaFree(ctx->ring);
-    if (ctx->ring_ctr) cudaFree(ctx->ring_ctr);
-    if (ctx->fuse_counters) cudaFree(ctx->fuse_counters);
     cudaGetLastError();
   }
   delete ctx;
 }
 
-void world_create(const Plan& plan, int device, Ctx** out) {
+// Emulated P-rank world in ONE process: rank r's context on devices[r % n].
+// With one device every rank's stages run in lockstep on one stream; with
+// several devices the ranks' exchange stores cross NVLink through direct
+// peer pointers and the sync points become cross-device event dependencies
+// issued by the host (no kernel ever waits on another).
+void world_create(const Plan& plan, const int* devices, int ndev, Ctx** out) {
   const int P = plan.nranks();
+  if (ndev < 1) raise(DFFTB_ConfigInvalid, "need at least one device");
   std::vector<Ctx*> ctxs(P, nullptr);
   try {
-    for (int r = 0; r < P; ++r) ctxs[r] = ctx_create(plan, r, device);
+    for (int r = 0; r < P; ++r) ctxs[r] = ctx_create(plan, r, devices[r % ndev]);
+    for (int a = 0; a < ndev; ++a)
+      for (int b = 0; b < ndev; ++b)
+        if (devices[a] != devices[b]) enable_peer(devices[a], devices[b]);
   } catch (...) {
     for (auto* c : ctxs) ctx_destroy(c);
     throw;
@@ -384,36 +445,49 @@ void world_create(const Plan& plan, int device, Ctx** out) {
   }
 }
 
-// ---------------------------------------------------------------- lowering
+// ---------------------------------------------------------------- programs
+
+enum class OpKind { Pass, Begin, Sync, Record, WaitEvent };
 
 struct Op {
-  bool barrier = false;
+  OpKind kind = OpKind::Pass;
+  int stream = 0;  // 0 caller's stream, 1 the context's side stream
+  // ---- pass
   bool tma = false;
   bool generic = false;  // non-power-of-two length: mixed-radix / Bluestein kernel
-  bool fused2 = false;   // two axes in one L2-resident plane pipeline (pb, fa below)
-  bool fwd2 = true;
-  PassParams pb{};
-  Fused2Args fa{};
-  GenParams g{};
-  TmaPlan tp{};
-  PassParams p{};
+  bool adj = false;      // lanes along a strided axis
+  bool remote = false;   // some destination is another rank's buffer
   int n = 1;
-  bool adj = false;
-  bool fused = false;
-  int grid_axis = 0;
-  std::vector<int> members;
-  // lane geometry (for pipelining): transform axis, lane axes, input layout
+  int grid_sms = 0;      // > 0: persistent grid limited to this many SMs (overlap split)
+  PassParams p{};
+  TmaPlan tp{};
+  GenParams g{};
+  // lane geometry (overlap chunking, spectral epilogue)
   int v = -1, ax_a = -1, ax_b = -1, ax_a1 = -1;
   const Dist* before = nullptr;
-  // pipelined pair: this op's pass (p, tp, adj) is the producer, (pb, tpb,
-  // adj_b) the consumer, on disjoint CTAs of one launch
-  bool pipe = false;
-  bool adj_b = false;
-  TmaPlan tpb{};
-  PipeArgs ppa{}, ppb{};
-  double frac = 0.5;
-  bool ring_reset = false;  // zero the ring counters before the launch
+  std::vector<int> members;  // exchange group (world ranks, group order)
+  // ---- sync point / events / begin
+  bool signal = false, wait = false;
+  int slot = 0;
+  int event = 0;
+  bool herm = false;  // Begin: clear the C2R statistics
 };
+
+struct Program {
+  std::vector<Op> ops;
+  bool c2r = false;
+  bool multi_stream = false;
+  int nevents = 0;
+  int uses = 0;  // the first run issues directly (kernel attributes set), later runs replay a graph
+  cudaGraphExec_t graph = nullptr;
+  bool graph_failed = false;
+};
+
+static void drop_programs(Ctx& ctx) {
+  for (auto& kv : ctx.programs)
+    if (kv.second->graph) cudaGraphExecDestroy(kv.second->graph);
+  ctx.programs.clear();
+}
 
 // Row-major element strides of a block; internal buffers pad the innermost
 // extent (inner_pad).
@@ -436,11 +510,6 @@ static void row_major_strides(const int64_t* len, int nd, int64_t* st, bool inte
   }
 }
 
-static bool zperm_enabled() {
-  const char* e = getenv("DFFTB_ZPERM");
-  return !(e && *e == '0');
-}
-
 static std::vector<int> group_members(const Dist& d, int me, int g) {
   auto c = d.coords_of(me);
   std::vector<int> m(d.grid[g]);
@@ -452,14 +521,14 @@ static std::vector<int> group_members(const Dist& d, int me, int g) {
   return m;
 }
 
-static void check_compatible(const Plan& plan, const Ctx& ctx) {
+static void check_compatible(const Plan& plan, Ctx& ctx) {
   if (plan.nranks() != ctx.nranks) raise(DFFTB_GridMismatch, "communicator size must match the grid");
-  if (plan.dims != ctx.dims || plan.grid != ctx.grid || plan.prec != ctx.prec ||
-      plan.decomp != ctx.decomp)
+  if (plan.dims != ctx.dims || plan.grid != ctx.grid || plan.prec != ctx.prec || plan.decomp != ctx.decomp)
     raise(DFFTB_GridMismatch, "context was made for a different plan geometry");
   if (!ctx.connected) raise(DFFTB_ConfigInvalid, "context is not connected to its peers");
-  if (family_bytes(plan) > ctx.exch_bytes)
-    raise(DFFTB_ArenaExhausted, "context buffers are too small for this plan");
+  if (std::find(ctx.checked_plans.begin(), ctx.checked_plans.end(), plan.id) != ctx.checked_plans.end()) return;
+  if (family_bytes(plan) > ctx.exch_bytes) raise(DFFTB_ArenaExhausted, "context buffers are too small for this plan");
+  ctx.checked_plans.push_back(plan.id);
 }
 
 static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
@@ -474,12 +543,8 @@ static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   return fn;
 }
 
-// L2 sector promotion of the strided-lane tensor maps (A/B aid:
-// DFFTB_L2PROMO = 0 none, 1 64 B, 2 128 B, 3 256 B (default))
 static CUtensorMapL2promotion l2_promotion() {
-  const char* e = getenv("DFFTB_L2PROMO");
-  const int v = e ? atoi(e) : 3;
-  switch (v) {
+  switch (knobs().l2promo) {
     case 0: return CU_TENSOR_MAP_L2_PROMOTION_NONE;
     case 1: return CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
     case 2: return CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
@@ -487,13 +552,13 @@ static CUtensorMapL2promotion l2_promotion() {
   }
 }
 
-static bool tma_disabled() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("DFFTB_NO_TMA");
-    v = (e && *e && *e != '0') ? 1 : 0;
-  }
-  return v == 1;
+// the whole pass as one launch box
+static void full_box(TmaArgs& a, const PassParams& p, int W) {
+  const int na = p.A * (p.A1 > 1 ? p.A1 : 1);
+  a.a0 = 0;
+  a.bt0 = 0;
+  a.nbt = (p.B + W - 1) / W;
+  a.ntiles = (int64_t)na * a.nbt;
 }
 
 // Decide whether a pass can use the TMA-prefetch kernel and build its
@@ -502,22 +567,14 @@ static bool tma_disabled() {
 static bool plan_tma(Op& op, int prec) {
   const PassParams& p = op.p;
   const int n = op.n;
-  if (tma_disabled() || n < 8 || (int64_t)p.A * p.B == 0) return false;
-  {
-    // debug aid: DFFTB_TMA_LK_MASK restricts the TMA path to some lane kinds
-    const char* m = getenv("DFFTB_TMA_LK_MASK");
-    const int lk = p.in_mode == kInReal ? kR2C
-                   : p.in_mode == kInHermitian ? kC2R
-                   : (p.inverse ? kC2CBwd : kC2CFwd);
-    if (m && *m && !((atoi(m) >> lk) & 1)) return false;
-  }
+  if (!knobs().tma || n < 8 || (int64_t)p.A * p.B == 0) return false;
   const int W = tma_tile_w(prec, n);
   if (W <= 0) return false;
   const int csize = 2 * prec;
   if ((reinterpret_cast<uintptr_t>(p.in) & 15) != 0) return false;
   TmaPlan& tp = op.tp;
   std::memset(&tp, 0, sizeof(tp));
-  tp.args.ntiles = (int64_t)p.A * (p.A1 > 1 ? p.A1 : 1) * ((p.B + W - 1) / W);
+  full_box(tp.args, p, W);
   if (p.A1 > 1 && (p.in_sa1 * (p.in_mode == kInReal ? prec : csize)) % 16) return false;
   if (op.adj) {
     if (p.in_mode != kInComplex) return false;
@@ -528,22 +585,10 @@ static bool plan_tma(Op& op, int prec) {
     if (si % 16 || sa % 16) {
       // rows a tensor map cannot describe (fp32 C2R user blocks: 129-bin
       // rows of 1032 bytes): per-thread 8-byte cp.async into the same tile
-      if (csize != 8 || (reinterpret_cast<uintptr_t>(p.in) & 7)) return false;
-      const char* e = getenv("DFFTB_UNALIGNED_LDGSTS");
-      if (e && *e == '0') return false;
+      if (csize != 8 || (reinterpret_cast<uintptr_t>(p.in) & 7) || !knobs().unaligned_ldgsts) return false;
       tp.args.bulk = 0;
       tp.args.ldgsts = 1;
       return true;
-    }
-    tp.args.bulk = 0;
-    {
-      // row loader: TMA boxes (default; measured faster even for 4-16 MB row
-      // strides) or per-thread cp.async (DFFTB_ADJ_LOADER=ldgsts|auto)
-      const char* e = getenv("DFFTB_ADJ_LOADER");
-      const std::string mode = e ? e : "tma";
-      // (16-byte cp.async per element: fp64 complex only)
-      tp.args.ldgsts = csize == 16 && (mode == "ldgsts" || (mode == "auto" && si >= (int64_t(1) << 20)));
-      if (tp.args.ldgsts) return true;
     }
     auto enc = tensor_map_encoder();
     if (!enc) return false;
@@ -570,10 +615,9 @@ static bool plan_tma(Op& op, int prec) {
       box[1] = 1;
       box[2] = rows;
     }
-    CUresult r = enc(&tp.tmap, prec == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
-                     3, const_cast<void*>(p.in), gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                     CU_TENSOR_MAP_SWIZZLE_NONE, l2_promotion(),
-                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    CUresult r = enc(&tp.tmap, prec == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+                     const_cast<void*>(p.in), gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_NONE, l2_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return false;
     tp.args.rows = rows;
     tp.args.bulk = 0;
@@ -605,7 +649,8 @@ static void set_store_mode(PassParams& p) {
   if ((b & (b - 1)) != 0 || p.dest[0].sk >= (1ll << 31)) return;
   for (int q = 1; q < p.ndest; ++q) {
     const Dest& d = p.dest[q];
-    if (d.base != p.dest[0].base || d.sa != p.dest[0].sa || d.sb != p.dest[0].sb || d.sk != p.dest[0].sk)
+    if (d.base != p.dest[0].base || d.sa != p.dest[0].sa || d.sb != p.dest[0].sb || d.sk != p.dest[0].sk ||
+        d.sa1 != p.dest[0].sa1)
       return;
   }
   p.store_mode = 1;
@@ -637,106 +682,18 @@ static void plan_generic(Op& op, const Ctx& ctx) {
   g.p.store_mode = 2;
 }
 
-// Merge "rows then columns" (forward) / "columns then rows" (backward) pass
-// pairs whose intermediate stays on this rank into one fused2 op: the
-// intermediate goes through the L2-resident plane ring instead of HBM.
-static void fuse_pairs(std::vector<Op>& prog, const Ctx& ctx) {
-  if (!ctx.fuse_ring) return;
-  const int prec = ctx.prec;
-  const int64_t csize = 2 * prec;
-  for (size_t i = 0; i + 1 < prog.size(); ++i) {
-    Op& a = prog[i];
-    const Op& b = prog[i + 1];
-    if (a.barrier || b.barrier || a.generic || b.generic || a.fused2) continue;
-    const PassParams& pa = a.p;
-    const PassParams& pb = b.p;
-    if (pa.in_mode != kInComplex || pb.in_mode != kInComplex || pa.out_real || pb.out_real) continue;
-    if (a.n != b.n || !fused2_supported(prec, a.n) || pa.ndest != 1) continue;
-    if (pa.dest[0].ptr != pb.in || pa.A != pb.A || pa.B != pb.B || pa.inverse != pb.inverse) continue;
-    if (pa.A1 > 1 || pb.A1 > 1) continue;
-    const bool fwd = !pa.inverse;
-    if (fwd ? (a.adj || !b.adj) : (!a.adj || b.adj)) continue;
-    if (!a.tma || (fwd ? !a.tp.args.bulk : (a.tp.args.bulk || a.tp.args.ldgsts))) continue;
-    const int n = a.n;
-    const int W = tma_tile_w(prec, n);
-    const int64_t plane = (int64_t)n * n;
-    const char* le = getenv("DFFTB_FUSE_L");
-    const char* lg = getenv("DFFTB_FUSE_LAG");
-    const int L = le ? std::max(2, atoi(le)) : 8;
-    const int lag = lg ? std::max(1, std::min(L - 1, atoi(lg))) : L / 2;
-    if ((size_t)(L * plane * csize) > ctx.fuse_ring_bytes || pa.A > ctx.fuse_planes) continue;
-    // small problems: the plane pipeline's dependency latency outweighs the
-    // saved round trip; keep the two plain passes
-    if (pa.A < 2 * L || (int64_t)pa.A * ((pa.B + W - 1) / W) < 4 * 148) continue;
-
-    Op f = a;
-    f.fused2 = true;
-    f.fwd2 = fwd;
-    // phase A: stores into ring slot (plane % L), scratch plane layout [x1][x2]
-    Dest& d = f.p.dest[0];
-    d.ptr = ctx.fuse_ring;
-    d.base = 0;
-    d.sa = plane;
-    d.sb = fwd ? n : 1;
-    d.sk = fwd ? 1 : n;
-    f.p.store_mode = 0;
-    f.p.oblk = n;
-    // phase B: reads the ring slot
-    f.pb = pb;
-    f.pb.in = ctx.fuse_ring;
-    f.pb.in_sa = plane;
-    f.pb.in_sb = fwd ? 1 : n;
-    f.pb.in_si = fwd ? n : 1;
-    Fused2Args& fa = f.fa;
-    std::memset(&fa, 0, sizeof(fa));
-    fa.P = pa.A;
-    fa.T = (pa.B + W - 1) / W;
-    fa.L = L;
-    fa.lag = lag;
-    fa.doneA = ctx.fuse_counters;
-    fa.doneB = ctx.fuse_counters + ctx.fuse_planes;
-    fa.ring = ctx.fuse_ring;
-    fa.persist_bytes = ctx.fuse_persist_bytes;
-    {
-      const char* nd = getenv("DFFTB_FUSE_NODEP");
-      fa.nodeps = nd && *nd == '1';
-    }
-    if (fwd) {
-      // contiguous phase A from the input rows, strided phase B from the ring
-      fa.lane_bytes = a.tp.args.lane_bytes;
-      auto enc = tensor_map_encoder();
-      if (!enc) continue;
-      const int rows = n < 256 ? n : 256;
-      cuuint64_t gdim[3] = {2 * (cuuint64_t)n, (cuuint64_t)n, (cuuint64_t)L};
-      cuuint64_t gstride[2] = {(cuuint64_t)(n * csize), (cuuint64_t)(plane * csize)};
-      cuuint32_t box[3] = {(cuuint32_t)(2 * W), (cuuint32_t)rows, 1}, estr[3] = {1, 1, 1};
-      if (enc(&f.tp.tmap, prec == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
-              ctx.fuse_ring, gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-              CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-        continue;
-      fa.rows = rows;
-      fa.i_dim = 1;
-    } else {
-      // strided phase A from the input (its own tensor map), contiguous B from the ring
-      fa.rows = a.tp.args.rows;
-      fa.i_dim = a.tp.args.i_dim;
-      fa.lane_bytes = (int)(n * csize);
-    }
-    prog[i] = f;
-    prog.erase(prog.begin() + i + 1);
-  }
-}
-
 // One local pass of a 3-D block: axis v of the buffer `in` (extents len,
 // element strides si) into `out` (strides so over the output extents).
-static Op single_pass(const Ctx& ctx, int v, int n, const int64_t* len, const int64_t* si,
-                      const void* in, void* out, const int64_t* so, int fkind, double scale) {
+static Op single_pass(const Ctx& ctx, int v, int n, const int64_t* len, const int64_t* si, const void* in,
+                      void* out, const int64_t* so, int fkind, double scale) {
   int lanes[2], nl = 0;
   for (int a = 0; a < 3; ++a)
     if (a != v) lanes[nl++] = a;
   const int ax_a = lanes[0], ax_b = lanes[1];
   Op op;
+  op.v = v;
+  op.ax_a = ax_a;
+  op.ax_b = ax_b;
   PassParams& p = op.p;
   p.in = in;
   p.A = (int)len[ax_a];
@@ -779,11 +736,7 @@ static Op single_pass(const Ctx& ctx, int v, int n, const int64_t* len, const in
 // user block at a whole-plane stride.  C2R keeps its Hermitian axis last.
 static bool lower_single(const Plan& plan, const Ctx& ctx, const void* d_in, void* d_out, int parity,
                          std::vector<Op>& prog) {
-  if (plan.nranks() != 1 || plan.input.ndim() != 3 || !zperm_enabled()) return false;
-  {
-    const char* e = getenv("DFFTB_SINGLE_REORDER");
-    if (e && *e == '0') return false;
-  }
+  if (plan.nranks() != 1 || plan.input.ndim() != 3 || !knobs().zperm || !knobs().single_reorder) return false;
   bool backward = false, c2r = false;
   double scale = 1.0;
   for (const auto& st : plan.stages) {
@@ -797,8 +750,8 @@ static bool lower_single(const Plan& plan, const Ctx& ctx, const void* d_in, voi
   }
   if (!backward) return false;
   int64_t off[3], lc[3], lr[3];
-  plan.input.extents_of(0, off, lc);    // complex (Hermitian for C2R) extents
-  plan.output.extents_of(0, off, lr);   // output extents
+  plan.input.extents_of(0, off, lc);   // complex (Hermitian for C2R) extents
+  plan.output.extents_of(0, off, lr);  // output extents
   for (int a = 0; a < 3; ++a)
     if (lc[a] <= 0) return false;
   const int prec = ctx.prec;
@@ -821,294 +774,10 @@ static bool lower_single(const Plan& plan, const Ctx& ctx, const void* d_in, voi
   return true;
 }
 
-// ------------------------------------------------------ pipelined pairs
-//
-// The reference overlaps communication with computation by chunking along
-// the N0/P0 planes (pipelined_all_to_all, exchange.hpp:250-423).
-// Here the two passes on either side of an exchange run concurrently on
-// disjoint CTAs of one launch, chunked along the lane axis both share (the
-// axis the exchange does not touch): while the NVLink-bound pass streams
-// chunk c to the peers, the HBM-bound pass already transforms chunk c - 1.
-// Per-chunk tile counters in every rank's flag page replace the group
-// barrier between the two passes.
-static constexpr int kPipeSlots = 8;
-static constexpr size_t kPipeOffU64 = 256;  // counter slots start after the barrier flags
-
-static bool pipe_candidate(const Op& o, int prec) {
-  if (o.barrier || o.generic || o.fused2 || o.pipe || !o.tma || o.before == nullptr) return false;
-  if (o.tp.args.ldgsts || o.p.A1 > 1 || o.p.A <= 0 || o.p.B <= 0) return false;
-  if (o.p.in_mode != kInComplex || o.p.out_real) return false;
-  return pipe_supported(prec, o.n);
-}
-
-static void pipeline_pairs(std::vector<Op>& prog, Ctx& ctx) {
-  // DFFTB_PIPE_LOCAL=1: also pair two local passes (profiling aid: lets the
-  // pipelined kernel run, and be profiled, on one GPU)
-  const char* pl = getenv("DFFTB_PIPE_LOCAL");
-  const bool local_pairs = pl && *pl == '1';
-  if (ctx.world_mode || (ctx.nranks < 2 && !local_pairs)) return;
-  {
-    // opt-in: measured slower than the sequential passes in round 1
-    const char* e = getenv("DFFTB_PIPE");
-    if (!(e && *e == '1') && !local_pairs) return;
-  }
-  int want = 16;
-  if (const char* e = getenv("DFFTB_PIPE_CHUNKS")) want = std::max(2, std::min(kMaxChunks, atoi(e)));
-  double frac_env = -1.0;
-  if (const char* e = getenv("DFFTB_PIPE_FRAC")) frac_env = atof(e);
-  if ((int)ctx.pipe_cum.size() < kPipeSlots) ctx.pipe_cum.assign(kPipeSlots, {});
-  const int me = ctx.rank;
-  const int prec = ctx.prec;
-  const int64_t csize = 2 * prec;
-  int slot = 0;
-  for (size_t i = 0; i + 1 < prog.size() && slot < kPipeSlots; ++i) {
-    Op& P = prog[i];
-    if (!pipe_candidate(P, prec)) continue;
-    size_t jq = i + 1;
-    const bool bar = prog[jq].barrier;
-    if (bar) ++jq;
-    if (jq >= prog.size()) continue;
-    Op& Q = prog[jq];
-    if (!pipe_candidate(Q, prec) || Q.n != P.n || Q.p.inverse != P.p.inverse) continue;
-    const bool p_remote = P.fused && P.members.size() > 1;
-    const bool q_remote = Q.fused && Q.members.size() > 1;
-    if (p_remote == q_remote && !(local_pairs && !p_remote)) continue;  // only NVLink next to HBM gains
-    // Q reads what P stored for this rank
-    int q_me = 0;
-    if (P.fused)
-      for (size_t q = 0; q < P.members.size(); ++q)
-        if (P.members[q] == me) q_me = (int)q;
-    if (P.p.dest[q_me].ptr != Q.p.in) continue;
-    if (P.before->ndim() != 3 || Q.before->ndim() != 3 || P.v == Q.v) continue;
-    const int X = 3 - P.v - Q.v;
-    if ((X != P.ax_a && X != P.ax_b) || (X != Q.ax_a && X != Q.ax_b)) continue;
-    const bool pbeta = X == P.ax_b, qbeta = X == Q.ax_b;
-    const int W = tma_tile_w(prec, P.n);
-    int64_t offP[kMaxDims], lenP[kMaxDims], offQ[kMaxDims], lenQ[kMaxDims];
-    P.before->extents_of(me, offP, lenP);
-    Q.before->extents_of(me, offQ, lenQ);
-    if (lenP[X] != lenQ[X] || offP[X] != offQ[X]) continue;
-    const int64_t Xe = lenP[X];
-    int64_t R = (Xe + want - 1) / want;
-    if (pbeta || qbeta) R = ((R + W - 1) / W) * W;
-    const int C = (int)((Xe + R - 1) / R);
-    if (C < 2 || C > kMaxChunks) continue;
-    auto tiles_b = [&](int64_t B) { return (B + W - 1) / W; };
-    auto tpc_of = [&](bool beta, int64_t A, int64_t B) { return beta ? (R / W) * A : R * tiles_b(B); };
-    auto in_chunk = [&](bool beta, int64_t A, int64_t B, int c) -> int64_t {
-      if (beta) {
-        const int64_t b0 = c * (R / W), b1 = std::min(b0 + R / W, tiles_b(B));
-        return std::max<int64_t>(0, b1 - b0) * A;
-      }
-      const int64_t a0 = c * R, a1 = std::min(a0 + R, A);
-      return std::max<int64_t>(0, a1 - a0) * tiles_b(B);
-    };
-    // every rank P writes into publishes there; the ranks writing into this
-    // rank's buffer are the same group (symmetric exchange)
-    std::vector<int> writers = p_remote ? P.members : std::vector<int>{me};
-    unsigned long long expect[kMaxChunks] = {};
-    for (int m : writers) {
-      int64_t o[kMaxDims], l[kMaxDims];
-      P.before->extents_of(m, o, l);
-      for (int c = 0; c < C; ++c) expect[c] += (unsigned long long)in_chunk(pbeta, l[P.ax_a], l[P.ax_b], c);
-    }
-    Op M = P;
-    M.pipe = true;
-    M.fused = true;
-    M.pb = Q.p;
-    M.tpb = Q.tp;
-    M.adj_b = Q.adj;
-    PipeArgs& pa = M.ppa;
-    PipeArgs& pq = M.ppb;
-    std::memset(&pa, 0, sizeof(pa));
-    std::memset(&pq, 0, sizeof(pq));
-    pa.order_beta = pbeta ? (int)(R / W) : 0;
-    pa.tpc = tpc_of(pbeta, P.p.A, P.p.B);
-    pa.pub_sys = p_remote;
-    const std::vector<int> targets = p_remote ? P.members : std::vector<int>{me};
-    pa.npub = (int)targets.size();
-    for (size_t q = 0; q < targets.size(); ++q)
-      pa.pub[q] = reinterpret_cast<unsigned long long*>(ctx.flags_of(targets[q])) + kPipeOffU64 +
-                  (size_t)slot * kMaxChunks;
-    pq.order_beta = qbeta ? (int)(R / W) : 0;
-    pq.tpc = tpc_of(qbeta, Q.p.A, Q.p.B);
-    pq.wait = reinterpret_cast<const unsigned long long*>(ctx.flags_of(me)) + kPipeOffU64 +
-              (size_t)slot * kMaxChunks;
-    for (int c = 0; c < C; ++c) {
-      ctx.pipe_cum[slot][c] += expect[c];
-      pq.target[c] = ctx.pipe_cum[slot][c];
-    }
-    pq.timeout_flag = ctx.dstat + 2;
-    pq.timeout_ns = 10ull * 1000 * 1000 * 1000;
-    // CTA split: balance max(SM-bound time, NVLink time) of the two roles
-    if (frac_env > 0.0 && frac_env < 1.0) {
-      M.frac = frac_env;
-    } else {
-      const double sm_rate = 40e9, nvl_rate = 700e9;  // B/s per SM (read + write), per GPU
-      auto role_time = [&](const Op& o, bool remote, double share) {
-        const double rw = 2.0 * (double)o.p.A * o.p.B * o.n * csize;
-        const double nvl = remote ? 0.5 * rw * (double)(o.members.size() - 1) / o.members.size() : 0.0;
-        return std::max(rw / (share * 148.0 * sm_rate), nvl / nvl_rate);
-      };
-      double best = 1e30;
-      for (int g = 8; g <= 140; ++g) {
-        const double f = g / 148.0;
-        const double t = std::max(role_time(P, p_remote, f), role_time(Q, q_remote, 1.0 - f));
-        if (t < best) {
-          best = t;
-          M.frac = f;
-        }
-      }
-    }
-    prog[i] = M;
-    prog.erase(prog.begin() + (long)jq);
-    if (bar) prog.erase(prog.begin() + (long)i + 1);
-    ++slot;
-  }
-}
-
-// Single GPU: the rows pass and the columns pass of every x0 plane run as
-// ONE pipelined launch whose intermediate lives in an L2-resident ring of
-// planes instead of a full buffer in HBM — two axes for one HBM round trip.
-// Producer CTAs transform rows into ring slot (plane % ring); consumer CTAs
-// wait for a chunk of planes, load it (TMA), drop the ring rows from L2
-// (discard: never written back) and transform the columns; the producer
-// reuses a slot once its chunk was consumed.  Counters are local and zeroed
-// before each launch (stream order), so no cross-execute bookkeeping.
-static constexpr int kRingMaxChunks = 4096;
-
-static bool ring_enabled() {
-  const char* e = getenv("DFFTB_RING");
-  return e && *e == '1';
-}
-
-static void ring_pairs(std::vector<Op>& prog, Ctx& ctx) {
-  if (ctx.world_mode || ctx.nranks != 1 || prog.size() < 2 || !ring_enabled()) return;
-  Op& P = prog[0];
-  Op& Q = prog[1];
-  const int prec = ctx.prec;
-  const int64_t csize = 2 * prec;
-  auto plain = [&](const Op& o) {
-    return !o.barrier && o.tma && !o.generic && !o.fused2 && !o.pipe && o.p.in_mode == kInComplex &&
-           !o.p.out_real && o.p.A1 <= 1 && o.p.A > 0 && o.p.B > 0 && !o.tp.args.ldgsts;
-  };
-  if (!plain(P) || !plain(Q) || P.n != Q.n || !pipe_supported(prec, P.n)) return;
-  if (P.adj || !Q.adj || P.p.inverse != Q.p.inverse) return;
-  if (P.p.ndest != 1 || P.p.store_mode != 0 || P.p.dest[0].ptr != Q.p.in) return;
-  if (P.p.A != Q.p.A || P.p.dest[0].sa != Q.p.in_sa || P.p.dest[0].base != 0 || Q.p.in_sb != 1) return;
-  const int W = tma_tile_w(prec, P.n);
-  int R = 2, L = 4;
-  if (const char* e = getenv("DFFTB_RING_R")) R = std::max(1, atoi(e));
-  if (const char* e = getenv("DFFTB_RING_L")) L = std::max(2, atoi(e));
-  double frac = 0.5;
-  if (const char* e = getenv("DFFTB_RING_FRAC")) frac = atof(e);
-  // Deadlock freedom: a CTA waits (for its prefetch, STAGES tiles ahead)
-  // while holding its current tiles unstored.  The producer's reuse lag must
-  // therefore exceed both roles' prefetch reach in chunks.
-  {
-    const int64_t tb = std::max<int64_t>((P.p.B + W - 1) / W, (Q.p.B + W - 1) / W);
-    const int np = std::max(1, (int)(frac * 148 + 0.5)), nq = std::max(1, 148 - np);
-    const int64_t reach = 2 * (int64_t)std::max(np, nq);  // STAGES = 2 tiles per CTA ahead
-    R = std::max<int64_t>(R, (reach + tb - 1) / tb);       // a chunk spans one reach
-    const int64_t tpc = (int64_t)R * ((std::min(P.p.B, Q.p.B) + W - 1) / W);
-    const int need = (int)((reach + tpc - 1) / tpc) * 2 + 2;
-    L = std::max(L, need);
-  }
-  const int A = P.p.A;
-  const int ringP = R * L;
-  const int C = (A + R - 1) / R;
-  if (A < 2 * ringP || C > kRingMaxChunks) return;
-  const size_t bytes = (size_t)ringP * (size_t)Q.p.in_sa * csize;
-  if (ctx.ring_bytes < bytes) {
-    if (ctx.ring) cudaFree(ctx.ring);
-    ctx.ring = nullptr;
-    ctx.ring_bytes = 0;
-    CUDA_TRY(cudaMalloc(&ctx.ring, bytes));
-    ctx.ring_bytes = bytes;
-  }
-  if (!ctx.ring_ctr) CUDA_TRY(cudaMalloc(&ctx.ring_ctr, 2 * kRingMaxChunks * sizeof(unsigned long long)));
-  // consumer's tensor map over the ring (same strides, ringP planes)
-  TmaPlan tq = Q.tp;
-  {
-    auto enc = tensor_map_encoder();
-    if (!enc) return;
-    const int64_t si = Q.p.in_si * csize, sa = Q.p.in_sa * csize;
-    cuuint64_t gdim[3] = {2 * (cuuint64_t)Q.p.B, 0, 0};
-    cuuint64_t gstride[2];
-    cuuint32_t box[3] = {(cuuint32_t)(2 * W), 0, 0}, estr[3] = {1, 1, 1};
-    const int rows = Q.tp.args.rows;
-    if (Q.tp.args.i_dim == 1) {
-      gdim[1] = Q.n;
-      gdim[2] = ringP;
-      gstride[0] = si;
-      gstride[1] = sa;
-      box[1] = rows;
-      box[2] = 1;
-    } else {
-      gdim[1] = ringP;
-      gdim[2] = Q.n;
-      gstride[0] = sa;
-      gstride[1] = si;
-      box[1] = 1;
-      box[2] = rows;
-    }
-    if (enc(&tq.tmap, prec == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, ctx.ring,
-            gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-      return;
-  }
-  const int64_t tbP = (P.p.B + W - 1) / W, tbQ = (Q.p.B + W - 1) / W;
-  const int64_t tpcP = (int64_t)R * tbP, tpcQ = (int64_t)R * tbQ;
-  unsigned long long* fwd_ctr = ctx.ring_ctr;
-  unsigned long long* back_ctr = ctx.ring_ctr + kRingMaxChunks;
-  Op M = P;
-  M.pipe = true;
-  M.ring_reset = true;
-  M.p.dest[0].ptr = ctx.ring;
-  M.pb = Q.p;
-  M.pb.in = ctx.ring;
-  M.tpb = tq;
-  M.adj_b = Q.adj;
-  PipeArgs& pa = M.ppa;
-  PipeArgs& pq = M.ppb;
-  std::memset(&pa, 0, sizeof(pa));
-  std::memset(&pq, 0, sizeof(pq));
-  pa.tpc = tpcP;
-  pa.npub = 1;
-  pa.pub[0] = fwd_ctr;
-  pa.ring = ringP;
-  pa.ring_role = 1;
-  pa.peer_tpc = tpcQ;
-  pa.peer_ntiles = Q.tp.args.ntiles;
-  pa.back_wait = back_ctr;
-  pa.back_lag = L;
-  pq.tpc = tpcQ;
-  pq.wait = fwd_ctr;
-  pq.ring = ringP;
-  pq.ring_role = 2;
-  pq.ring_discard = (int64_t)W * csize == 128 ? 1 : 0;
-  if (const char* e = getenv("DFFTB_RING_DISCARD")) pq.ring_discard = pq.ring_discard && *e != '0';
-  pq.peer_tpc = tpcP;
-  pq.peer_ntiles = P.tp.args.ntiles;
-  pq.back_pub = back_ctr;
-  for (PipeArgs* x : {&pa, &pq}) {
-    x->timeout_flag = ctx.dstat + 2;
-    x->timeout_ns = 10ull * 1000 * 1000 * 1000;
-  }
-  M.frac = frac;
-  prog[0] = M;
-  prog.erase(prog.begin() + 1);
-}
-
-// One rank's program: fused passes and barriers.  `peer` supplies the
-// exchange-buffer base of any world rank (its own mapping of the peers).
-static std::vector<Op> lower(const Plan& plan, Ctx& ctx, const void* d_in, void* d_out,
-                             int parity) {
+// One rank's program: fused passes and sync points, in stage order.
+static std::vector<Op> lower(const Plan& plan, const Ctx& ctx, const void* d_in, void* d_out, int parity) {
   std::vector<Op> prog;
-  if (lower_single(plan, ctx, d_in, d_out, parity, prog)) {
-    ring_pairs(prog, ctx);
-    return prog;
-  }
+  if (lower_single(plan, ctx, d_in, d_out, parity, prog)) return prog;
   const int me = ctx.rank;
   const void* cur = d_in;
   bool cur_internal = false;  // d_in has the user layout; exch/work are padded
@@ -1166,17 +835,15 @@ static std::vector<Op> lower(const Plan& plan, Ctx& ctx, const void* d_in, void*
     op.adj = p.in_si != 1;
     if (lenb[v] == 0 && st.fkind != DFFTB_C2R) p.A = 0;
 
-    op.tma = false;
     if (tr) {
       const Dist& Lo = tr->after;
       const int g = tr->grid_axis;
       const int u = tr->before.axis_of_grid[g];
       // the transposed final forward exchange feeds the axis-0 pass: store
       // its buffer [x1][x0][rest] so axis-0 lanes read short strides
-      const bool swap_out = tr->transposed && zperm_enabled() && nd >= 3;
-      op.fused = true;
-      op.grid_axis = g;
+      const bool swap_out = tr->transposed && knobs().zperm && nd >= 3;
       op.members = group_members(Lo, me, g);
+      op.remote = op.members.size() > 1;
       p.ndest = (int)op.members.size();
       p.oblk = (Lo.dims[v] + Lo.grid[g] - 1) / Lo.grid[g];
       for (int q = 0; q < p.ndest; ++q) {
@@ -1196,11 +863,13 @@ static std::vector<Op> lower(const Plan& plan, Ctx& ctx, const void* d_in, void*
       op.tma = plan_tma(op, ctx.prec);
       plan_generic(op, ctx);
       prog.push_back(op);
-      Op b;
-      b.barrier = true;
-      b.grid_axis = g;
-      b.members = op.members;
-      if (b.members.size() > 1) prog.push_back(b);
+      if (op.remote) {
+        Op b;
+        b.kind = OpKind::Sync;
+        b.signal = b.wait = true;
+        b.members = op.members;
+        prog.push_back(b);
+      }
       cur = ctx.exch(me, slot, parity);
       cur_internal = true;
       cur_swap01 = swap_out;
@@ -1218,7 +887,7 @@ static std::vector<Op> lower(const Plan& plan, Ctx& ctx, const void* d_in, void*
       d.ptr = out;
       d.base = 0;
       d.sa = ax_a >= 0 ? so[ax_a] : 0;
-        d.sa1 = ax_a1 >= 0 ? so[ax_a1] : 0;
+      d.sa1 = ax_a1 >= 0 ? so[ax_a1] : 0;
       d.sb = so[ax_b];
       d.sk = so[v];
       set_store_mode(p);
@@ -1231,58 +900,179 @@ static std::vector<Op> lower(const Plan& plan, Ctx& ctx, const void* d_in, void*
       i += nm ? 2 : 1;
     }
   }
-  fuse_pairs(prog, ctx);
-  pipeline_pairs(prog, ctx);
-  ring_pairs(prog, ctx);
   return prog;
 }
 
-static void launch_op(const Ctx& ctx, const Op& op, uint64_t epoch, cudaStream_t s) {
-  if (op.barrier) {
-    if (ctx.world_mode) return;  // lockstep emulation: stream order is the barrier
-    BarrierParams bp{};
-    bp.nmem = (int)op.members.size();
-    for (int i = 0; i < bp.nmem; ++i) {
-      bp.members[i] = op.members[i];
-      bp.peer_flags[i] = reinterpret_cast<unsigned long long*>(ctx.flags_of(op.members[i]));
+// ----------------------------------------------------------------- overlap
+//
+// [P: exchange pass] [sync] [Q: local pass] -> chunks c = 0..C-1 along the
+// lane axis X both passes share (neither transforms it, and the exchange does
+// not redistribute it, so every group member's chunk c covers the same global
+// X range).  P's chunk c stores, then signals sync point k_c to the group;
+// Q's chunk c waits for P's chunk c locally (event) and for the group's
+// signals (remote), on the side stream.  The SMs are split so the two run
+// concurrently: P needs enough to keep NVLink busy, Q takes the rest.
+
+static bool overlap_candidate(const Op& o) {
+  return o.kind == OpKind::Pass && o.tma && !o.generic && o.before && o.before->ndim() == 3 && o.p.A1 <= 1 &&
+         o.p.A > 0 && o.p.B > 0;
+}
+
+// SM share of the exchange pass: both passes finish together when
+// max(P's HBM-pass time on g SMs, its NVLink time) = Q's time on 148 - g SMs.
+static int overlap_split(const Op& P, const Op& Q, int prec, int sms) {
+  if (knobs().frac > 0.0 && knobs().frac < 1.0) return std::max(1, (int)(knobs().frac * sms + 0.5));
+  const double csize = 2.0 * prec;
+  const double hbm = 6.2e12, nvl = 0.70e12;  // measured pass rate and NVLink store rate (B200)
+  auto bytes = [&](const Op& o) {
+    const double lanes = (double)o.p.A * o.p.B;
+    const double in_e = o.p.in_mode == kInReal ? 0.5 : 1.0, out_e = o.p.out_real ? 0.5 : 1.0;
+    return lanes * (o.n * in_e + o.p.n_out * out_e) * csize;
+  };
+  const double tp = bytes(P) / hbm, tq = bytes(Q) / hbm;
+  const double remote = (double)P.p.A * P.p.B * P.p.n_out * csize * (double)(P.members.size() - 1) /
+                        (double)P.members.size();
+  const double tn = remote / nvl;
+  int best = sms / 2;
+  double bt = 1e30;
+  for (int g = 8; g <= sms - 8; ++g) {
+    const double t = std::max(std::max(tp * sms / g, tn), tq * sms / (sms - g));
+    if (t < bt) {
+      bt = t;
+      best = g;
     }
-    bp.me = ctx.rank;
-    bp.my_flags = reinterpret_cast<unsigned long long*>(ctx.flags_of(ctx.rank));
-    bp.epoch = epoch;
-    bp.timeout_ns = kBarrierTimeoutNs;
-    bp.timeout_flag = ctx.dstat + 2;
-    CUDA_TRY(launch_barrier(bp, s));
-    return;
   }
-  if ((int64_t)op.p.A * op.p.B == 0) return;
-  if (op.fused2) {
-    CUDA_TRY(cudaMemsetAsync(op.fa.doneA, 0, 2 * sizeof(unsigned int) * op.fa.P, s));
-    CUDA_TRY(launch_fused2(ctx.prec, op.n, op.fwd2, op.p, op.pb, op.tp.tmap, op.fa, s));
-    return;
+  return best;
+}
+
+// chunk c of a pass as a launch box (X on the alpha or the beta axis)
+static TmaArgs chunk_box(const Op& o, int X, int64_t x0, int64_t x1, int W) {
+  TmaArgs a = o.tp.args;
+  const int nbt_all = (o.p.B + W - 1) / W;
+  if (X == o.ax_a) {
+    a.a0 = (int)x0;
+    a.bt0 = 0;
+    a.nbt = nbt_all;
+    a.ntiles = (x1 - x0) * (int64_t)nbt_all;
+  } else {
+    a.a0 = 0;
+    a.bt0 = (int)(x0 / W);
+    a.nbt = (int)((x1 - x0 + W - 1) / W);
+    a.ntiles = (int64_t)o.p.A * a.nbt;
   }
-  if (op.pipe) {
-    if (op.ring_reset)
-      CUDA_TRY(cudaMemsetAsync(ctx.ring_ctr, 0, 2 * kRingMaxChunks * sizeof(unsigned long long), s));
-    CUDA_TRY(launch_pipe(ctx.prec, op.n, op.p, op.adj, op.tp, op.ppa, op.pb, op.adj_b, op.tpb, op.ppb, op.frac, s));
-    const char* dbg = getenv("DFFTB_RING_DEBUG");
-    if (op.ring_reset && dbg && *dbg == '1') {
-      std::vector<unsigned long long> h(2 * kRingMaxChunks);
-      CUDA_TRY(cudaMemcpyAsync(h.data(), ctx.ring_ctr, h.size() * 8, cudaMemcpyDeviceToHost, s));
-      CUDA_TRY(cudaStreamSynchronize(s));
-      const int C = (int)((op.tp.args.ntiles + op.ppa.tpc - 1) / op.ppa.tpc);
-      fprintf(stderr, "[ring] tpcP %lld ntP %lld tpcQ %lld ntQ %lld chunks %d ring %d lag %d frac %.2f\n",
-              (long long)op.ppa.tpc, (long long)op.tp.args.ntiles, (long long)op.ppb.tpc,
-              (long long)op.tpb.args.ntiles, C, op.ppa.ring, op.ppa.back_lag, op.frac);
-      for (int c = 0; c < C; ++c)
-        if (c < 6 || c > C - 3 || h[c] != (unsigned long long)op.ppa.tpc ||
-            h[kRingMaxChunks + c] != (unsigned long long)op.ppb.tpc)
-          fprintf(stderr, "[ring] chunk %d produced %llu consumed %llu\n", c, h[c], h[kRingMaxChunks + c]);
+  return a;
+}
+
+static void overlap_pairs(std::vector<Op>& prog, const Plan& plan, const Ctx& ctx, int& nevents) {
+  if (!knobs().overlap || ctx.world_mode || ctx.nranks < 2) return;
+  int C = knobs().chunks;
+  if (plan.options.exchange == DFFTB_EXCHANGE_PIPELINED && plan.options.chunks_per_peer > 1)
+    C = std::min(16, plan.options.chunks_per_peer);
+  if (C < 2) return;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx.device);
+  const int me = ctx.rank;
+  std::vector<Op> out;
+  size_t i = 0;
+  while (i < prog.size()) {
+    const bool pattern = i + 2 < prog.size() && overlap_candidate(prog[i]) && prog[i].remote &&
+                         prog[i + 1].kind == OpKind::Sync && overlap_candidate(prog[i + 2]) &&
+                         !prog[i + 2].remote && prog[i + 2].p.ndest == 1;
+    if (!pattern) {
+      out.push_back(prog[i++]);
+      continue;
     }
-    return;
+    const Op& P = prog[i];
+    const Op& S = prog[i + 1];
+    const Op& Q = prog[i + 2];
+    const int X = 3 - P.v - Q.v;
+    bool ok = P.v != Q.v && X >= 0 && X < 3 && (X == P.ax_a || X == P.ax_b) && (X == Q.ax_a || X == Q.ax_b);
+    int64_t offQ[kMaxDims], lenQ[kMaxDims];
+    if (ok) {
+      Q.before->extents_of(me, offQ, lenQ);
+      for (int m : P.members) {
+        int64_t o[kMaxDims], l[kMaxDims];
+        P.before->extents_of(m, o, l);
+        ok = ok && o[X] == offQ[X] && l[X] == lenQ[X];
+      }
+    }
+    const int WP = tma_tile_w(ctx.prec, P.n), WQ = tma_tile_w(ctx.prec, Q.n);
+    const int64_t Xe = ok ? lenQ[X] : 0;
+    // chunk length: a whole number of tiles on the beta axis of either pass
+    int64_t unit = 1;
+    if (ok && X == P.ax_b) unit = std::max<int64_t>(unit, WP);
+    if (ok && X == Q.ax_b) unit = std::max<int64_t>(unit, WQ);
+    int64_t R = ok ? ((Xe + C - 1) / C + unit - 1) / unit * unit : 0;
+    const int nch = R > 0 ? (int)((Xe + R - 1) / R) : 0;
+    if (!ok || nch < 2 || P.tp.args.ldgsts || Q.tp.args.ldgsts) {
+      out.push_back(prog[i++]);
+      continue;
+    }
+    const int gP = overlap_split(P, Q, ctx.prec, sms);
+    for (int c = 0; c < nch; ++c) {
+      const int64_t x0 = c * R, x1 = std::min<int64_t>(Xe, x0 + R);
+      Op pc = P;
+      pc.tp.args = chunk_box(P, X, x0, x1, WP);
+      pc.grid_sms = gP;
+      out.push_back(pc);
+      Op sig;
+      sig.kind = OpKind::Sync;
+      sig.signal = true;
+      sig.members = S.members;
+      out.push_back(sig);
+      Op rec;
+      rec.kind = OpKind::Record;
+      rec.event = nevents + c;
+      out.push_back(rec);
+      Op we;
+      we.kind = OpKind::WaitEvent;
+      we.stream = 1;
+      we.event = nevents + c;
+      out.push_back(we);
+      Op wt;
+      wt.kind = OpKind::Sync;
+      wt.stream = 1;
+      wt.wait = true;
+      wt.members = S.members;
+      out.push_back(wt);  // signal and wait of chunk c share a sync slot (assign_slots)
+      Op qc = Q;
+      qc.stream = 1;
+      qc.tp.args = chunk_box(Q, X, x0, x1, WQ);
+      qc.grid_sms = sms - gP;
+      out.push_back(qc);
+    }
+    // join: the caller's stream waits for the side stream
+    Op rj;
+    rj.kind = OpKind::Record;
+    rj.stream = 1;
+    rj.event = nevents + nch;
+    out.push_back(rj);
+    Op wj;
+    wj.kind = OpKind::WaitEvent;
+    wj.event = nevents + nch;
+    out.push_back(wj);
+    nevents += nch + 1;
+    i += 3;
   }
-  if (op.generic) CUDA_TRY(launch_generic(ctx.prec, op.g, s));
-  else if (op.tma) CUDA_TRY(launch_pass_tma(ctx.prec, op.n, op.p, op.adj, op.tp, s));
-  else CUDA_TRY(launch_pass(ctx.prec, op.n, op.p, op.adj, s));
+  prog.swap(out);
+}
+
+// Sync slots: every barrier gets its own slot; the signal of chunk c and the
+// wait that follows it share one.
+static void assign_slots(std::vector<Op>& prog) {
+  int next = 0, open_signal = -1;
+  for (auto& o : prog) {
+    if (o.kind != OpKind::Sync) continue;
+    if (o.signal && o.wait) {
+      o.slot = next++;
+    } else if (o.signal) {
+      o.slot = next++;
+      open_signal = o.slot;
+    } else {
+      o.slot = open_signal;
+    }
+  }
+  if (next > kSyncSlots) raise(DFFTB_Unsupported, "too many sync points in one program");
 }
 
 static bool plan_has_c2r(const Plan& plan) {
@@ -1291,10 +1081,229 @@ static bool plan_has_c2r(const Plan& plan) {
   return false;
 }
 
-static void validate_finite(const Plan& plan, const Ctx& ctx, const void* d_in, cudaStream_t s) {
+static std::shared_ptr<Program> build_program(const Plan& plan, Ctx& ctx, const void* d_in, void* d_out,
+                                              int parity) {
+  auto pr = std::make_shared<Program>();
+  std::vector<Op> ops = lower(plan, ctx, d_in, d_out, parity);
+  overlap_pairs(ops, plan, ctx, pr->nevents);
+  assign_slots(ops);
+  pr->c2r = plan_has_c2r(plan);
+  bool has_sync = false;
+  for (const auto& o : ops) {
+    has_sync = has_sync || o.kind == OpKind::Sync;
+    pr->multi_stream = pr->multi_stream || o.stream != 0;
+  }
+  if (pr->c2r || (has_sync && !ctx.world_mode)) {
+    Op b;
+    b.kind = OpKind::Begin;
+    b.herm = pr->c2r;
+    pr->ops.push_back(b);
+  }
+  for (auto& o : ops) pr->ops.push_back(std::move(o));
+  return pr;
+}
+
+static cudaEvent_t event_at(Ctx& ctx, int i) {
+  while ((int)ctx.events.size() <= i) {
+    cudaEvent_t e;
+    CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ctx.events.push_back(e);
+  }
+  return static_cast<cudaEvent_t>(ctx.events[i]);
+}
+
+static SyncParams sync_params(const Ctx& ctx, const Op& op) {
+  SyncParams sp{};
+  sp.nmem = (int)op.members.size();
+  for (int i = 0; i < sp.nmem; ++i) {
+    sp.members[i] = op.members[i];
+    sp.peer_flags[i] = reinterpret_cast<unsigned long long*>(ctx.flags_of(op.members[i]));
+  }
+  sp.me = ctx.rank;
+  sp.slot = op.slot;
+  sp.signal = op.signal;
+  sp.wait = op.wait;
+  sp.my_flags = reinterpret_cast<unsigned long long*>(ctx.flags_of(ctx.rank));
+  sp.epoch = ctx.dstat + kStatEpoch;
+  sp.timeout_ns = kSyncTimeoutNs;
+  sp.timeout_flag = ctx.dstat + 2;
+  return sp;
+}
+
+// Issue one op.  `s` = the caller's stream (or the capture stream).
+static void launch_op(Ctx& ctx, const Op& op, cudaStream_t s) {
+  cudaStream_t st = op.stream ? static_cast<cudaStream_t>(ctx.side) : s;
+  switch (op.kind) {
+    case OpKind::Begin:
+      CUDA_TRY(launch_sync_begin(ctx.dstat + kStatEpoch, op.herm ? ctx.dstat : nullptr, st));
+      return;
+    case OpKind::Sync:
+      if (ctx.world_mode) return;  // lockstep emulation: ordering comes from the host
+      CUDA_TRY(launch_sync_point(sync_params(ctx, op), st));
+      return;
+    case OpKind::Record:
+      CUDA_TRY(cudaEventRecord(event_at(ctx, op.event), st));
+      return;
+    case OpKind::WaitEvent:
+      CUDA_TRY(cudaStreamWaitEvent(st, event_at(ctx, op.event), 0));
+      return;
+    case OpKind::Pass:
+      break;
+  }
+  if ((int64_t)op.p.A * op.p.B == 0) return;
+  if (op.generic) CUDA_TRY(launch_generic(ctx.prec, op.g, st));
+  else if (op.tma) {
+    if (op.tp.args.ntiles > 0) CUDA_TRY(launch_pass_tma(ctx.prec, op.n, op.p, op.adj, op.tp, op.grid_sms, st));
+  } else CUDA_TRY(launch_pass(ctx.prec, op.n, op.p, op.adj, st));
+}
+
+// The side stream joins the caller's stream at the start of a program (it
+// must not run ahead of what the caller enqueued before).
+static void fork_side(Ctx& ctx, const Program& pr, cudaStream_t s) {
+  if (!pr.multi_stream) return;
+  cudaEvent_t e = event_at(ctx, pr.nevents);
+  CUDA_TRY(cudaEventRecord(e, s));
+  CUDA_TRY(cudaStreamWaitEvent(static_cast<cudaStream_t>(ctx.side), e, 0));
+}
+
+static void issue_program(Ctx& ctx, Program& pr, cudaStream_t s) {
+  fork_side(ctx, pr, s);
+  for (const auto& op : pr.ops) launch_op(ctx, op, s);
+}
+
+// Replay through a CUDA graph (captured on first use).  Falls back to direct
+// issue if capture is not possible (e.g. the caller's stream is itself being
+// captured).
+static void run_graph(Ctx& ctx, Program& pr, cudaStream_t s) {
+  if (pr.uses++ == 0) {
+    issue_program(ctx, pr, s);
+    return;
+  }
+  if (!pr.graph && !pr.graph_failed) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &cs);
+    if (cs != cudaStreamCaptureStatusNone) {
+      issue_program(ctx, pr, s);
+      return;
+    }
+    cudaStream_t cap = static_cast<cudaStream_t>(ctx.capture);
+    cudaGraph_t graph = nullptr;
+    CUDA_TRY(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+    try {
+      issue_program(ctx, pr, cap);
+    } catch (...) {
+      cudaStreamEndCapture(cap, &graph);
+      if (graph) cudaGraphDestroy(graph);
+      cudaGetLastError();
+      throw;
+    }
+    cudaError_t e = cudaStreamEndCapture(cap, &graph);
+    if (e == cudaSuccess && graph) e = cudaGraphInstantiate(&pr.graph, graph, 0);
+    if (graph) cudaGraphDestroy(graph);
+    if (e != cudaSuccess || !pr.graph) {
+      cudaGetLastError();
+      pr.graph = nullptr;
+      pr.graph_failed = true;
+    }
+  }
+  if (pr.graph) CUDA_TRY(cudaGraphLaunch(pr.graph, s));
+  else issue_program(ctx, pr, s);
+}
+
+static std::string program_key(const Plan& plan, const void* d_in, const void* d_out, int parity,
+                               const char* extra = "") {
+  char buf[160];
+  snprintf(buf, sizeof(buf), "%llu:%p:%p:%d:%s", (unsigned long long)plan.id, d_in, d_out, parity, extra);
+  return buf;
+}
+
+static Program& cached_program(const Plan& plan, Ctx& ctx, const void* d_in, void* d_out, int parity,
+                               const std::string& key) {
+  auto it = ctx.programs.find(key);
+  if (it != ctx.programs.end()) return *it->second;
+  if (ctx.programs.size() >= kMaxCachedPrograms) drop_programs(ctx);
+  auto pr = build_program(plan, ctx, d_in, d_out, parity);
+  return *ctx.programs.emplace(key, pr).first->second;
+}
+
+// Per-op device times (TimingBreakdown, timing.hpp:16-37): local passes ->
+// local_fft; exchange passes (FFT with the pack / all_to_all / unpack fused
+// into their stores) and sync points -> wire_comm; pack, unpack and
+// staging_copy stay 0 (no separate passes exist).  Ops on the side stream
+// overlap the caller's, so the components may sum to more than `total`.
+static void run_timed(Ctx& ctx, Program& pr, cudaStream_t s, dfftb_timing* timers) {
+  struct Mark {
+    cudaEvent_t a, b;
+    const Op* op;
+  };
+  std::vector<Mark> marks;
+  cudaEvent_t t0, t1;
+  CUDA_TRY(cudaEventCreate(&t0));
+  CUDA_TRY(cudaEventCreate(&t1));
+  CUDA_TRY(cudaEventRecord(t0, s));
+  fork_side(ctx, pr, s);
+  for (const auto& op : pr.ops) {
+    const bool timed = op.kind == OpKind::Pass || (op.kind == OpKind::Sync && !ctx.world_mode);
+    cudaStream_t st = op.stream ? static_cast<cudaStream_t>(ctx.side) : s;
+    Mark m{nullptr, nullptr, &op};
+    if (timed) {
+      CUDA_TRY(cudaEventCreate(&m.a));
+      CUDA_TRY(cudaEventCreate(&m.b));
+      CUDA_TRY(cudaEventRecord(m.a, st));
+    }
+    launch_op(ctx, op, s);
+    if (timed) {
+      CUDA_TRY(cudaEventRecord(m.b, st));
+      marks.push_back(m);
+    }
+  }
+  CUDA_TRY(cudaEventRecord(t1, s));
+  CUDA_TRY(cudaEventSynchronize(t1));
+  std::memset(timers, 0, sizeof(*timers));
+  ctx.last_ops.clear();
+  for (auto& m : marks) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, m.a, m.b);
+    const double sec = ms * 1e-3;
+    OpTime ot{};
+    ot.stream = m.op->stream;
+    ot.ms = ms;
+    if (m.op->kind == OpKind::Sync) {
+      ot.kind = 2;
+      timers->wire_comm += sec;
+    } else if (m.op->remote) {
+      ot.kind = 1;
+      ot.n = m.op->n;
+      timers->wire_comm += sec;
+    } else {
+      ot.kind = 0;
+      ot.n = m.op->n;
+      timers->local_fft += sec;
+    }
+    ctx.last_ops.push_back(ot);
+    cudaEventDestroy(m.a);
+    cudaEventDestroy(m.b);
+  }
+  float ms = 0;
+  cudaEventElapsedTime(&ms, t0, t1);
+  timers->total = ms * 1e-3;
+  cudaEventDestroy(t0);
+  cudaEventDestroy(t1);
+  if (knobs().op_times) {
+    static const char* kinds[3] = {"local", "exchange", "sync"};
+    for (const auto& o : ctx.last_ops)
+      fprintf(stderr, "[dfftb rank %d] %s%s n=%d: %.3f ms\n", ctx.rank, kinds[o.kind], o.stream ? " (side)" : "",
+              o.n, o.ms);
+  }
+}
+
+static void launch_validate(const Plan& plan, const Ctx& ctx, const void* d_in, cudaStream_t s) {
   const int64_t n = plan.input.local_count(ctx.rank) * (plan.input.complex_el ? 2 : 1);
   CUDA_TRY(cudaMemsetAsync(ctx.dstat + 3, 0, sizeof(unsigned long long), s));
   CUDA_TRY(launch_nonfinite(plan.prec, d_in, n, ctx.dstat + 3, s));
+}
+
+static void check_validate(const Ctx& ctx, cudaStream_t s) {
   unsigned long long bad = 0;
   CUDA_TRY(cudaMemcpyAsync(&bad, ctx.dstat + 3, sizeof(bad), cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaStreamSynchronize(s));
@@ -1308,7 +1317,7 @@ void ctx_check(Ctx& ctx, cudaStream_t s) {
   CUDA_TRY(cudaStreamSynchronize(s));
   if (st[2]) {
     CUDA_TRY(cudaMemset(ctx.dstat + 2, 0, sizeof(unsigned long long)));
-    raise(DFFTB_Deadlock, "peer did not reach the exchange barrier (timeout)");
+    raise(DFFTB_Deadlock, "peer did not reach the exchange sync point (timeout)");
   }
   if (ctx.c2r_pending) {
     ctx.c2r_pending = false;
@@ -1317,113 +1326,130 @@ void ctx_check(Ctx& ctx, cudaStream_t s) {
     std::memcpy(&im, &st[1], sizeof(double));
     // irfft_1d tolerance, kernels.hpp:348-377 (scale = block max, plan.hpp:440-446)
     const double tol = (ctx.prec == 8 ? 1e-6 : 1e-2) * mx;
-    const char* skip = getenv("DFFTB_DEBUG_SKIP_HERM");
-    if (im > tol && !(skip && *skip == '1')) {
+    if (im > tol) {
       char buf[160];
-      snprintf(buf, sizeof(buf),
-               "DC or Nyquist bin has a non-real component (|Im| %.3g > tol %.3g, block max %.3g)",
+      snprintf(buf, sizeof(buf), "DC or Nyquist bin has a non-real component (|Im| %.3g > tol %.3g, block max %.3g)",
                im, tol, mx);
       raise(DFFTB_NonHermitian, buf);
     }
   }
 }
 
-struct EventTimer {
-  std::vector<cudaEvent_t> ev;
-  ~EventTimer() {
-    for (auto e : ev) cudaEventDestroy(e);
-  }
-  void mark(cudaStream_t s) {
-    cudaEvent_t e;
-    cudaEventCreate(&e);
-    cudaEventRecord(e, s);
-    ev.push_back(e);
-  }
-};
-
-static void run_program(const Plan& plan, Ctx& ctx, const std::vector<Op>& prog, cudaStream_t s, int flags,
-                        dfftb_timing* timers);
-
-void execute(const Plan& plan, Ctx& ctx, const void* d_in, void* d_out, cudaStream_t s, int flags,
-             dfftb_timing* timers) {
-  DeviceGuard g(ctx.device);
-  check_compatible(plan, ctx);
-  if (plan.options.validate_finite) validate_finite(plan, ctx, d_in, s);
-  const int parity = (int)(ctx.exec_count & 1);
-  ctx.exec_count++;
-  auto prog = lower(plan, ctx, d_in, d_out, parity);
-  run_program(plan, ctx, prog, s, flags, timers);
-}
-
-static void run_program(const Plan& plan, Ctx& ctx, const std::vector<Op>& prog, cudaStream_t s, int flags,
-                        dfftb_timing* timers) {
-  if (plan_has_c2r(plan)) {
-    CUDA_TRY(cudaMemsetAsync(ctx.dstat, 0, 2 * sizeof(unsigned long long), s));
-    ctx.c2r_pending = true;
-  }
-  EventTimer et;
-  if (timers) et.mark(s);
-  for (const auto& op : prog) {
-    const uint64_t epoch = op.barrier ? ++ctx.epoch : 0;
-    launch_op(ctx, op, epoch, s);
-    if (timers) et.mark(s);
-  }
-  if (timers) {
-    CUDA_TRY(cudaStreamSynchronize(s));
-    std::memset(timers, 0, sizeof(*timers));
-    for (size_t k = 0; k < prog.size(); ++k) {
-      float ms = 0;
-      cudaEventElapsedTime(&ms, et.ev[k], et.ev[k + 1]);
-      const double sec = ms * 1e-3;
-      if (prog[k].barrier || prog[k].fused) timers->wire_comm += sec;
-      else timers->local_fft += sec;
-    }
-    float ms = 0;
-    cudaEventElapsedTime(&ms, et.ev.front(), et.ev.back());
-    timers->total = ms * 1e-3;
-    // profiling aid: DFFTB_OP_TIMES=1 prints every op of the program
-    const char* ot = getenv("DFFTB_OP_TIMES");
-    if (ot && *ot == '1') {
-      for (size_t k = 0; k < prog.size(); ++k) {
-        float m = 0;
-        cudaEventElapsedTime(&m, et.ev[k], et.ev[k + 1]);
-        const Op& o = prog[k];
-        fprintf(stderr, "[dfftb rank %d] op %zu %s n=%d A=%d B=%d dests=%d: %.3f ms\n", ctx.rank, k,
-                o.barrier ? "barrier" : (o.pipe ? "pipe" : (o.fused ? "fused-exchange" : "local")), o.n, o.p.A,
-                o.p.B, o.p.ndest, m);
-      }
-    }
-  }
+// Every rank issues the whole program even when its input fails validation
+// (the check is reported after the launches), so the ranks' sync points and
+// buffer parities never drift apart.
+static void run_program(const Plan& plan, Ctx& ctx, Program& pr, cudaStream_t s, int flags, dfftb_timing* timers,
+                        bool validate) {
+  if (pr.c2r) ctx.c2r_pending = true;
+  if (timers) run_timed(ctx, pr, s, timers);
+  else if (knobs().graphs) run_graph(ctx, pr, s);
+  else issue_program(ctx, pr, s);
+  if (validate) check_validate(ctx, s);
   if (timers || (flags & DFFTB_EXEC_SYNC)) ctx_check(ctx, s);
 }
 
-void execute_world(const Plan& plan, Ctx** ctxs, const void* const* d_in, void* const* d_out,
-                   cudaStream_t s, int flags) {
+void execute(const Plan& plan, Ctx& ctx, const void* d_in, void* d_out, cudaStream_t s, int flags,
+             dfftb_timing* timers) {
+  NvtxRange nr("dfftb_execute");
+  DeviceGuard g(ctx.device);
+  check_compatible(plan, ctx);
+  if (ctx.world_mode) raise(DFFTB_ConfigInvalid, "emulated-world contexts run through execute_world");
+  const bool validate = plan.options.validate_finite;
+  if (validate) launch_validate(plan, ctx, d_in, s);
+  const int parity = (int)(ctx.exec_count & 1);
+  ctx.exec_count++;
+  Program& pr = cached_program(plan, ctx, d_in, d_out, parity, program_key(plan, d_in, d_out, parity));
+  run_program(plan, ctx, pr, s, flags, timers, validate);
+}
+
+// Lockstep issue of all ranks' programs.  One device: stream order is the
+// barrier.  Several devices: each rank runs on its context's side stream and
+// every sync point becomes "record on every member's stream, wait on them".
+static void check_world(const Plan& plan, Ctx** ctxs) {
   const int P = plan.nranks();
-  std::vector<std::vector<Op>> progs(P);
   for (int r = 0; r < P; ++r) {
     if (!ctxs[r]->world_mode) raise(DFFTB_ConfigInvalid, "not an emulated world");
     check_compatible(plan, *ctxs[r]);
     if (ctxs[r]->rank != r) raise(DFFTB_InvalidRank, "world contexts must be in rank order");
   }
-  DeviceGuard g(ctxs[0]->device);
-  for (int r = 0; r < P; ++r) {
-    if (plan.options.validate_finite) validate_finite(plan, *ctxs[r], d_in[r], s);
-    const int parity = (int)(ctxs[r]->exec_count & 1);
-    ctxs[r]->exec_count++;
-    progs[r] = lower(plan, *ctxs[r], d_in[r], d_out[r], parity);
-    if (plan_has_c2r(plan)) {
-      CUDA_TRY(cudaMemsetAsync(ctxs[r]->dstat, 0, 2 * sizeof(unsigned long long), s));
-      ctxs[r]->c2r_pending = true;
+}
+
+static void run_world(const Plan& plan, Ctx** ctxs, const std::vector<Program*>& progs, cudaStream_t s,
+                      int flags) {
+  const int P = plan.nranks();
+  bool multi_dev = false;
+  for (int r = 1; r < P; ++r) multi_dev = multi_dev || ctxs[r]->device != ctxs[0]->device;
+  for (int r = 0; r < P; ++r)
+    if (progs[r]->c2r) ctxs[r]->c2r_pending = true;
+  const size_t nops = progs[0]->ops.size();
+  for (int r = 1; r < P; ++r)
+    if (progs[r]->ops.size() != nops) raise(DFFTB_CountMismatch, "rank programs differ in length");
+  auto stream_of = [&](int r) { return multi_dev ? static_cast<cudaStream_t>(ctxs[r]->side) : s; };
+  if (multi_dev) {
+    // every rank's stream starts after what the caller enqueued on s
+    cudaEvent_t e = event_at(*ctxs[0], 0);
+    {
+      DeviceGuard g(ctxs[0]->device);
+      CUDA_TRY(cudaEventRecord(e, s));
+    }
+    for (int r = 0; r < P; ++r) {
+      DeviceGuard g(ctxs[r]->device);
+      CUDA_TRY(cudaStreamWaitEvent(stream_of(r), e, 0));
     }
   }
-  const size_t nops = progs[0].size();
-  for (int r = 1; r < P; ++r)
-    if (progs[r].size() != nops) raise(DFFTB_CountMismatch, "rank programs differ in length");
-  for (size_t k = 0; k < nops; ++k)
-    for (int r = 0; r < P; ++r) launch_op(*ctxs[r], progs[r][k], 0, s);
+  for (size_t k = 0; k < nops; ++k) {
+    if (multi_dev && progs[0]->ops[k].kind == OpKind::Sync) {
+      for (int r = 0; r < P; ++r) {
+        DeviceGuard g(ctxs[r]->device);
+        CUDA_TRY(cudaEventRecord(event_at(*ctxs[r], 1), stream_of(r)));
+      }
+      for (int r = 0; r < P; ++r) {
+        DeviceGuard g(ctxs[r]->device);
+        for (int m : progs[r]->ops[k].members)
+          if (m != r) CUDA_TRY(cudaStreamWaitEvent(stream_of(r), event_at(*ctxs[m], 1), 0));
+      }
+      continue;
+    }
+    for (int r = 0; r < P; ++r) {
+      DeviceGuard g(ctxs[r]->device);
+      launch_op(*ctxs[r], progs[r]->ops[k], stream_of(r));
+    }
+  }
+  if (multi_dev) {
+    for (int r = 0; r < P; ++r) {
+      DeviceGuard g(ctxs[r]->device);
+      CUDA_TRY(cudaEventRecord(event_at(*ctxs[r], 2), stream_of(r)));
+    }
+    DeviceGuard g(ctxs[0]->device);
+    for (int r = 0; r < P; ++r) CUDA_TRY(cudaStreamWaitEvent(s, event_at(*ctxs[r], 2), 0));
+  }
+  if (plan.options.validate_finite)
+    for (int r = 0; r < P; ++r) {
+      DeviceGuard g(ctxs[r]->device);
+      check_validate(*ctxs[r], stream_of(r));
+    }
   if (flags & DFFTB_EXEC_SYNC)
-    for (int r = 0; r < P; ++r) ctx_check(*ctxs[r], s);
+    for (int r = 0; r < P; ++r) {
+      DeviceGuard g(ctxs[r]->device);
+      ctx_check(*ctxs[r], stream_of(r));
+    }
+}
+
+void execute_world(const Plan& plan, Ctx** ctxs, const void* const* d_in, void* const* d_out, cudaStream_t s,
+                   int flags) {
+  NvtxRange nr("dfftb_execute_world");
+  check_world(plan, ctxs);
+  const int P = plan.nranks();
+  std::vector<Program*> progs(P);
+  for (int r = 0; r < P; ++r) {
+    DeviceGuard g(ctxs[r]->device);
+    Ctx& c = *ctxs[r];
+    if (plan.options.validate_finite) launch_validate(plan, c, d_in[r], s);
+    const int parity = (int)(c.exec_count & 1);
+    c.exec_count++;
+    progs[r] = &cached_program(plan, c, d_in[r], d_out[r], parity, program_key(plan, d_in[r], d_out[r], parity));
+  }
+  run_world(plan, ctxs, progs, s, flags);
 }
 
 void fill_seeded(const Plan& plan, int rank, int side, uint64_t seed, int complex_field, void* d_buf,
@@ -1444,9 +1470,16 @@ void fill_seeded(const Plan& plan, int rank, int side, uint64_t seed, int comple
   CUDA_TRY(launch_seeded(plan.prec, sp, d_buf, s));
 }
 
-}  // namespace dfftb
-
-namespace dfftb {
+int last_op_times(const Ctx& ctx, int* kinds, int* streams, int* lengths, double* ms, int max) {
+  const int n = (int)ctx.last_ops.size();
+  for (int i = 0; i < n && i < max; ++i) {
+    if (kinds) kinds[i] = ctx.last_ops[i].kind;
+    if (streams) streams[i] = ctx.last_ops[i].stream;
+    if (lengths) lengths[i] = ctx.last_ops[i].n;
+    if (ms) ms[i] = ctx.last_ops[i].ms;
+  }
+  return n;
+}
 
 // ------------------------------------------------------- spectral operators
 
@@ -1468,8 +1501,14 @@ static SpectralParams spectral_params(const Plan& plan, int rank, const double* 
   return sp;
 }
 
-void spectral_apply(const Plan& plan, int rank, int op, int axis, const double* lengths, const void* in,
-                    void* out, int accumulate, cudaStream_t s) {
+static void check_zero_mean(const Plan& plan, const double v[2]) {
+  double total = 1;
+  for (auto d : plan.dims) total *= (double)d;
+  if (std::hypot(v[0], v[1]) > 1e-12 * total) raise(DFFTB_NonZeroMean, "inverse_laplacian needs a zero-mean field");
+}
+
+void spectral_apply(const Plan& plan, int rank, int op, int axis, const double* lengths, const void* in, void* out,
+                    int accumulate, cudaStream_t s) {
   SpectralParams sp = spectral_params(plan, rank, lengths);
   if (op < 0 || op > 2) raise(DFFTB_ConfigInvalid, "unknown spectral operator");
   if (op == 0 && (axis < 0 || axis >= sp.nd)) raise(DFFTB_OutOfRange, "derivative axis out of range");
@@ -1492,99 +1531,164 @@ void spectral_apply(const Plan& plan, int rank, int op, int axis, const double* 
         v[0] = fv[0];
         v[1] = fv[1];
       }
-      double total = 1;
-      for (auto d : plan.dims) total *= (double)d;
-      if (std::hypot(v[0], v[1]) > 1e-12 * total)
-        raise(DFFTB_NonZeroMean, "inverse_laplacian needs a zero-mean field");
+      check_zero_mean(plan, v);
     }
   }
   CUDA_TRY(launch_spectral(plan.prec, sp, in, out, s));
 }
 
-// Forward transform with the spectral multiplier fused into the last pass's
-// store epilogue: one read + one write of the spectrum
-// less than execute + spectral_apply, bit-identical results.  Lengths the
-// generic (non-power-of-two) kernel handles take the two-step path.
-void execute_spectral(const Plan& plan, Ctx& ctx, const void* d_in, void* d_out, int op, int axis,
-                      const double* lengths, int accumulate, cudaStream_t s, int flags) {
-  DeviceGuard dg(ctx.device);
-  check_compatible(plan, ctx);
-  if (ctx.world_mode) raise(DFFTB_ConfigInvalid, "execute_spectral needs a per-rank context (not an emulated world)");
+// The forward program of `plan` with the spectral multiplier fused into the
+// store epilogue of its last pass: one read + one
+// write of the spectrum less than execute + spectral_apply, bit-identical
+// values.  Returns a program with no ops when the last pass cannot carry the
+// epilogue (non-power-of-two last axis): the caller runs the two-step path.
+static Program& spectral_program(const Plan& plan, Ctx& ctx, const void* d_in, void* d_out, int parity, int op,
+                                 int axis, const double* lengths, int accumulate) {
   const SpectralParams sp = spectral_params(plan, ctx.rank, lengths);
+  char extra[160];
+  snprintf(extra, sizeof(extra), "spec%d:%d:%d:%.17g:%.17g:%.17g:%.17g", op, axis, accumulate,
+           lengths ? lengths[0] : -1.0, lengths && sp.nd > 1 ? lengths[1] : -1.0,
+           lengths && sp.nd > 2 ? lengths[2] : -1.0, lengths && sp.nd > 3 ? lengths[3] : -1.0);
+  const std::string key = program_key(plan, d_in, d_out, parity, extra);
+  auto it = ctx.programs.find(key);
+  if (it != ctx.programs.end()) return *it->second;
+  if (ctx.programs.size() >= kMaxCachedPrograms) drop_programs(ctx);
+  auto pr = build_program(plan, ctx, d_in, d_out, parity);
+  Op* last = nullptr;
+  for (auto& o : pr->ops)
+    if (o.kind == OpKind::Pass) last = &o;
+  const bool fusable = last && !last->generic && last->before && last->p.ndest == 1 &&
+                       last->p.dest[0].ptr == d_out && !last->p.inverse && last->p.in_mode == kInComplex &&
+                       !last->p.out_real;
+  if (fusable) {
+    SpecEpi& e = last->p.spec;
+    std::memset(&e, 0, sizeof(e));
+    e.op = op + 1;
+    e.accumulate = accumulate;
+    const int roles[4] = {last->v, last->ax_a, last->ax_b, last->ax_a1};
+    int64_t off[kMaxDims], len[kMaxDims];
+    last->before->extents_of(ctx.rank, off, len);
+    bool owns_dc = true;
+    for (int r = 0; r < 4; ++r) {
+      const int a = roles[r];
+      if (a < 0) {
+        // absent lane axis (2-D): a zero coordinate of a length-1 axis
+        e.off[r] = 0;
+        e.n[r] = 1;
+        e.half[r] = 0;
+        e.scale[r] = 0.0;
+        continue;
+      }
+      e.off[r] = r == 0 ? 0 : off[a];
+      e.n[r] = sp.n[a];
+      e.half[r] = sp.half[a];
+      e.scale[r] = sp.scale[a];
+      if (op == 0 && a == axis) e.deriv_role = r;
+      if (r > 0 && off[a] != 0) owns_dc = false;
+    }
+    // |k|^2 summed in tensor-axis order (as spectral_kernel): bit-identical
+    int nro = 0;
+    for (int a = 0; a < sp.nd; ++a)
+      for (int r = 0; r < 4; ++r)
+        if (roles[r] == a) e.order[nro++] = r;
+    e.nroles = nro;
+    // the multiplier variant exists for the strided-lane TMA kernel only
+    if (last->tma && !last->adj) last->tma = false;
+    if (op == 2 && owns_dc && sp.count > 0) e.dc = ctx.dstat + 4;
+  } else {
+    pr->ops.clear();  // marks the two-step path (forward + multiply kernel)
+  }
+  return *ctx.programs.emplace(key, pr).first->second;
+}
+
+static void check_spectral_args(const Plan& plan, int rank, int op, int axis, const double* lengths) {
+  const SpectralParams sp = spectral_params(plan, rank, lengths);
   if (op < 0 || op > 2) raise(DFFTB_ConfigInvalid, "unknown spectral operator");
   if (op == 0 && (axis < 0 || axis >= sp.nd)) raise(DFFTB_OutOfRange, "derivative axis out of range");
-  if (plan.options.validate_finite) validate_finite(plan, ctx, d_in, s);
+}
+
+static const Op* last_pass(const Program& pr) {
+  const Op* last = nullptr;
+  for (const auto& o : pr.ops)
+    if (o.kind == OpKind::Pass) last = &o;
+  return last;
+}
+
+static void read_dc_check(const Plan& plan, const Ctx& ctx, cudaStream_t s) {
+  unsigned long long bits[2];
+  CUDA_TRY(cudaMemcpyAsync(bits, ctx.dstat + 4, sizeof(bits), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  double v[2];
+  std::memcpy(v, bits, sizeof(v));
+  check_zero_mean(plan, v);
+}
+
+void execute_spectral(const Plan& plan, Ctx& ctx, const void* d_in, void* d_out, int op, int axis,
+                      const double* lengths, int accumulate, cudaStream_t s, int flags) {
+  NvtxRange nr("dfftb_execute_spectral");
+  DeviceGuard dg(ctx.device);
+  check_compatible(plan, ctx);
+  if (ctx.world_mode) raise(DFFTB_ConfigInvalid, "emulated-world contexts run through execute_world_spectral");
+  check_spectral_args(plan, ctx.rank, op, axis, lengths);
+  const bool validate = plan.options.validate_finite;
+  if (validate) launch_validate(plan, ctx, d_in, s);
   const int parity = (int)(ctx.exec_count & 1);
   ctx.exec_count++;
-  auto prog = lower(plan, ctx, d_in, d_out, parity);
-  Op* last = prog.empty() ? nullptr : &prog.back();
-  const bool fusable = last && !last->barrier && !last->generic && !last->fused2 && !last->pipe &&
-                       last->before && last->p.ndest == 1 && last->p.dest[0].ptr == d_out &&
-                       !last->p.inverse && last->p.in_mode == kInComplex && !last->p.out_real;
-  const char* nf = getenv("DFFTB_SPECTRAL_UNFUSED");
-  if (!fusable || (nf && *nf == '1')) {
-    run_program(plan, ctx, prog, s, 0, nullptr);
+  Program& pr = spectral_program(plan, ctx, d_in, d_out, parity, op, axis, lengths, accumulate);
+  if (pr.ops.empty()) {
+    Program& fw = cached_program(plan, ctx, d_in, d_out, parity, program_key(plan, d_in, d_out, parity));
+    run_program(plan, ctx, fw, s, 0, nullptr, validate);
     spectral_apply(plan, ctx.rank, op, axis, lengths, d_out, d_out, accumulate, s);
     if (flags & DFFTB_EXEC_SYNC) ctx_check(ctx, s);
     return;
   }
-  SpecEpi& e = last->p.spec;
-  std::memset(&e, 0, sizeof(e));
-  e.op = op + 1;
-  e.accumulate = accumulate;
-  const int roles[4] = {last->v, last->ax_a, last->ax_b, last->ax_a1};
-  int64_t off[kMaxDims], len[kMaxDims];
-  last->before->extents_of(ctx.rank, off, len);
-  e.nroles = 0;
-  bool owns_dc = true;
-  for (int r = 0; r < 4; ++r) {
-    const int a = roles[r];
-    if (a < 0) {
-      // absent lane axis (2-D): a zero coordinate of a length-1 axis
-      e.off[r] = 0;
-      e.n[r] = 1;
-      e.half[r] = 0;
-      e.scale[r] = 0.0;
-      continue;
-    }
-    e.nroles = r + 1;
-    e.off[r] = r == 0 ? 0 : off[a];
-    e.n[r] = sp.n[a];
-    e.half[r] = sp.half[a];
-    e.scale[r] = sp.scale[a];
-    if (op == 0 && a == axis) e.deriv_role = r;
-    if (r > 0 && off[a] != 0) owns_dc = false;
-  }
-  // |k|^2 summed in tensor-axis order (as spectral_kernel): bit-identical
-  {
-    int n = 0;
-    for (int a = 0; a < sp.nd; ++a)
-      for (int r = 0; r < 4; ++r)
-        if (roles[r] == a) e.order[n++] = r;
-    e.nroles = n;
-  }
-  if (last->tma) {
-    // the multiplier variant exists for the strided-lane kernel only
-    if (!last->adj) last->tma = false;
-  }
-  const bool check_mean = op == 2 && owns_dc && sp.count > 0;
-  if (check_mean) {
-    CUDA_TRY(cudaMemsetAsync(ctx.dstat + 4, 0, 2 * sizeof(unsigned long long), s));
-    e.dc = ctx.dstat + 4;
-  }
-  run_program(plan, ctx, prog, s, 0, nullptr);
-  if (check_mean) {
-    unsigned long long bits[2];
-    CUDA_TRY(cudaMemcpyAsync(bits, ctx.dstat + 4, sizeof(bits), cudaMemcpyDeviceToHost, s));
-    CUDA_TRY(cudaStreamSynchronize(s));
-    double v[2];
-    std::memcpy(v, bits, sizeof(v));
-    double total = 1;
-    for (auto d : plan.dims) total *= (double)d;
-    if (std::hypot(v[0], v[1]) > 1e-12 * total)
-      raise(DFFTB_NonZeroMean, "inverse_laplacian needs a zero-mean field");
-  }
+  const bool check_mean = last_pass(pr)->p.spec.dc != nullptr;
+  if (check_mean) CUDA_TRY(cudaMemsetAsync(ctx.dstat + 4, 0, 2 * sizeof(unsigned long long), s));
+  run_program(plan, ctx, pr, s, 0, nullptr, validate);
+  if (check_mean) read_dc_check(plan, ctx, s);
   if (flags & DFFTB_EXEC_SYNC) ctx_check(ctx, s);
+}
+
+// The emulated world's execute_spectral: every rank's fused program in
+// lockstep (or, for non-fusable plans, execute_world + per-rank multiply).
+void execute_world_spectral(const Plan& plan, Ctx** ctxs, const void* const* d_in, void* const* d_out, int op,
+                            int axis, const double* lengths, int accumulate, cudaStream_t s, int flags) {
+  NvtxRange nr("dfftb_execute_world_spectral");
+  check_world(plan, ctxs);
+  const int P = plan.nranks();
+  for (int r = 0; r < P; ++r) check_spectral_args(plan, r, op, axis, lengths);
+  std::vector<Program*> progs(P);
+  bool fused = true;
+  for (int r = 0; r < P; ++r) {
+    DeviceGuard g(ctxs[r]->device);
+    Ctx& c = *ctxs[r];
+    if (plan.options.validate_finite) launch_validate(plan, c, d_in[r], s);
+    const int parity = (int)(c.exec_count & 1);
+    c.exec_count++;
+    progs[r] = &spectral_program(plan, c, d_in[r], d_out[r], parity, op, axis, lengths, accumulate);
+    fused = fused && !progs[r]->ops.empty();
+    if (progs[r]->ops.empty() || last_pass(*progs[r])->p.spec.dc)
+      CUDA_TRY(cudaMemsetAsync(c.dstat + 4, 0, 2 * sizeof(unsigned long long), s));
+  }
+  if (!fused) {
+    for (int r = 0; r < P; ++r) {
+      Ctx& c = *ctxs[r];
+      const int parity = (int)((c.exec_count - 1) & 1);
+      progs[r] = &cached_program(plan, c, d_in[r], d_out[r], parity, program_key(plan, d_in[r], d_out[r], parity));
+    }
+  }
+  run_world(plan, ctxs, progs, s, 0);
+  for (int r = 0; r < P; ++r) {
+    DeviceGuard g(ctxs[r]->device);
+    cudaStream_t st = ctxs[r]->device == ctxs[0]->device ? s : static_cast<cudaStream_t>(ctxs[r]->side);
+    if (!fused) spectral_apply(plan, r, op, axis, lengths, d_out[r], d_out[r], accumulate, st);
+    else if (last_pass(*progs[r])->p.spec.dc) read_dc_check(plan, *ctxs[r], st);
+  }
+  if (flags & DFFTB_EXEC_SYNC)
+    for (int r = 0; r < P; ++r) {
+      DeviceGuard g(ctxs[r]->device);
+      ctx_check(*ctxs[r], ctxs[r]->device == ctxs[0]->device ? s : static_cast<cudaStream_t>(ctxs[r]->side));
+    }
 }
 
 void wavenumbers(const Plan& plan, int rank, int axis, int deriv, const double* lengths, double* k_out) {

@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(256) fft_generic_kernel(const __grid_constant_
   const int beta0 = (blockIdx.x - alpha * tiles_b) * W;
   const bool adj = p.in_si != 1;
   const int lane_len = p.in_mode == kInHermitian ? n / 2 + 1 : n;
-  T lmax = T(0), limag = T(0);
+  double lmax = 0.0, limag = 0.0;
 
   // ---- load (lane semantics as in the Stockham pass), coalesced mapping
   for (int e = threadIdx.x; e < W * n; e += blockDim.x) {
@@ -128,11 +128,11 @@ __global__ void __launch_bounds__(256) fft_generic_kernel(const __grid_constant_
         const bool lo = i <= n / 2;
         x = reinterpret_cast<const C*>(p.in)[lane + (int64_t)(lo ? i : n - i) * p.in_si];
         if (lo) {
-          const T m = sqrt(x.x * x.x + x.y * x.y);
+          const double m = hypot((double)x.x, (double)x.y);
           lmax = m > lmax ? m : lmax;
         }
         if (i == 0 || (n % 2 == 0 && i == n / 2)) {
-          limag = fabs(x.y) > limag ? fabs(x.y) : limag;
+          limag = fabs((double)x.y) > limag ? fabs((double)x.y) : limag;
           x.y = T(0);
         }
         if (!lo) x.y = -x.y;  // Hermitian mirror
@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(256) fft_generic_kernel(const __grid_constant_
     }
   }
   __syncthreads();
-  if (p.in_mode == kInHermitian) herm_reduce<T>(p.herm, lmax, limag);
+  if (p.in_mode == kInHermitian) herm_reduce(p.herm, lmax, limag);
 
   C* r = generic_fft<T>(a, b, g);
   if (g.bluestein) {

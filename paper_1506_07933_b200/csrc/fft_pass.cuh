@@ -42,12 +42,6 @@
 #ifndef DFFTB_TMA_THREADS
 #define DFFTB_TMA_THREADS 512  // threads per CTA of the TMA pass kernel
 #endif
-#ifndef DFFTB_EXP_NOCOMPUTE
-#define DFFTB_EXP_NOCOMPUTE 0  // timing experiment: skip the butterflies (wrong results)
-#endif
-#ifndef DFFTB_EXP_NOSTORE
-#define DFFTB_EXP_NOSTORE 0  // timing experiment: skip the global stores
-#endif
 #ifndef DFFTB_TWB
 #define DFFTB_TWB 1  // twiddle bases kept in registers across tiles
 #endif
@@ -402,7 +396,7 @@ __device__ __forceinline__ void run_stages(Cpx<T>* v, Cpx<T>* lane, const Cpx<T>
 // backward transforms.  Accumulates the C2R check statistics.
 template <typename T, int N, int EPREF, class LDC, class LDR>
 __device__ __forceinline__ void fetch0(Cpx<T>* v, int j, bool active, int in_mode, int inverse,
-                                       LDC ldc, LDR ldr, T& local_max, T& local_imag) {
+                                       LDC ldc, LDR ldr, double& local_max, double& local_imag) {
   using C = Cpx<T>;
   using SC = Sched<N, EPREF>;
   constexpr int E = SC::E;
@@ -424,11 +418,11 @@ __device__ __forceinline__ void fetch0(Cpx<T>* v, int j, bool active, int in_mod
           const int src = pos <= N / 2 ? pos : N - pos;
           x = ldc(src);
           if (pos <= N / 2) {
-            const T m = sqrt(x.x * x.x + x.y * x.y);
+            const double m = hypot((double)x.x, (double)x.y);
             local_max = m > local_max ? m : local_max;
           }
           if (pos == 0 || pos == N / 2) {
-            const T im = fabs(x.y);
+            const double im = fabs((double)x.y);
             local_imag = im > local_imag ? im : local_imag;
             x.y = T(0);
           }
@@ -443,8 +437,7 @@ __device__ __forceinline__ void fetch0(Cpx<T>* v, int j, bool active, int in_mod
 
 // block max-abs and DC/Nyquist imaginary residue (irfft_1d checks,
 // kernels.hpp:369-377, with the block scale of plan.hpp:440-446)
-template <typename T>
-__device__ __forceinline__ void herm_reduce(unsigned long long* herm, T local_max, T local_imag) {
+__device__ __forceinline__ void herm_reduce(unsigned long long* herm, double local_max, double local_imag) {
   unsigned long long mb = dbits(local_max), ib = dbits(local_imag);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -530,13 +523,13 @@ __global__ void __launch_bounds__(W* Sched<N, EPREF>::TPL, DFFTB_MINB)
   const C* tw = reinterpret_cast<const C*>(p.tw);
   const int64_t lane_off = in_alpha_off(p, alpha) + (int64_t)beta * p.in_sb;
   C v[SC::E];
-  T lmax = T(0), limag = T(0);
+  double lmax = 0.0, limag = 0.0;
   fetch0<T, N, EPREF>(
       v, j, active, p.in_mode, p.inverse,
       [&](int pos) { return __ldg(reinterpret_cast<const C*>(p.in) + lane_off + (int64_t)pos * p.in_si); },
       [&](int pos) { return __ldg(reinterpret_cast<const T*>(p.in) + lane_off + (int64_t)pos * p.in_si); },
       lmax, limag);
-  if (p.in_mode == kInHermitian) herm_reduce<T>(p.herm, lmax, limag);
+  if (p.in_mode == kInHermitian) herm_reduce(p.herm, lmax, limag);
   run_stages<T, N, EPREF, 0>(v, lane, tw, j);
   if (active) store_out<T, N, EPREF>(p, v, j, alpha, beta);
 }

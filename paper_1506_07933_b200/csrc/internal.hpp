@@ -108,6 +108,16 @@ struct CtxHandle {
 };
 static_assert(sizeof(CtxHandle) == 128, "handle must stay 128 bytes");
 
+struct Program;  // exec.cu: one rank's lowered, cached program
+
+// per-op device time of the last timed execute (dfftb_ctx_last_ops)
+struct OpTime {
+  int kind;    // 0 local pass, 1 exchange pass (remote stores), 2 sync point
+  int stream;  // 0 caller's stream, 1 side stream (overlapped consumer)
+  int n;       // transform length (passes)
+  double ms;
+};
+
 struct Ctx {
   int rank = 0;
   int nranks = 1;
@@ -118,37 +128,37 @@ struct Ctx {
   int decomp = DFFTB_PENCIL;
   int kind_family = 0;  // 0 C2C, 1 R2C/C2R
 
-  // one device region, IPC-exported: [flags][exch0 p0][exch0 p1][exch1 p0][exch1 p1]
+  // one device region, IPC-exported: [flag page][slot0 p0][slot0 p1][slot1 p0]...
   void* region = nullptr;
   size_t region_bytes = 0;
   size_t flags_bytes = 0;
   size_t exch_bytes = 0;
+  int exch_slots = 2;    // exchange buffers per parity in the shared region
   void* work = nullptr;  // private scratch for local->local passes
   size_t work_bytes = 0;
-  unsigned long long* dstat = nullptr;  // [0] herm max, [1] herm imag, [2] timeout flag, [3] nonfinite
-  void* fuse_ring = nullptr;            // L2-resident plane ring of the fused two-axis pass
-  size_t fuse_ring_bytes = 0;
-  size_t fuse_persist_bytes = 0;        // persisting-L2 carve-out reserved for the ring
-  unsigned int* fuse_counters = nullptr;  // [2 * fuse_planes]
-  int fuse_planes = 0;
-  std::map<int, void*> twiddles;        // N -> device table (prec of the ctx)
+  size_t table_bytes = 0;  // twiddle + Bluestein tables
+  // [0] herm max bits, [1] herm imag bits, [2] timeout flag, [3] nonfinite
+  // count, [4..5] DC bin of inverse_laplacian, [6] device epoch
+  unsigned long long* dstat = nullptr;
+  std::map<int, void*> twiddles;                     // N -> device table (prec of the ctx)
   std::map<int, std::pair<void*, void*>> bluestein;  // n -> (chirp, kernel spectrum)
 
   std::vector<void*> peer_region;  // per world rank, mapped into this process
   std::vector<bool> peer_opened;   // opened through cudaIpcOpenMemHandle
   bool connected = false;
-  bool world_mode = false;
-  uint64_t epoch = 0;
+  bool world_mode = false;         // lockstep emulation (execute_world)
   uint64_t exec_count = 0;
-  // pipelined pass pairs: cumulative per-chunk counter targets of each
-  // counter slot (identical on every rank: all ranks run the same programs)
-  std::vector<std::array<unsigned long long, 32>> pipe_cum;
-  // single-GPU L2 plane ring of the fused rows->columns pass pair
-  void* ring = nullptr;
-  size_t ring_bytes = 0;
-  int exch_slots = 2;  // exchange buffers per parity in the shared region
-  unsigned long long* ring_ctr = nullptr;  // [2 * kRingMaxChunks]: produced, consumed
   bool c2r_pending = false;
+
+  // streams and events of the overlapped exchange (side stream = consumer
+  // pass of a pipelined pair) and of graph capture
+  void* side = nullptr;     // cudaStream_t
+  void* capture = nullptr;  // cudaStream_t
+  std::vector<void*> events;  // cudaEvent_t pool, grown on demand
+  // cached programs: key (plan id, buffers, parity, epilogue) -> program
+  std::map<std::string, std::shared_ptr<Program>> programs;
+  std::vector<uint64_t> checked_plans;  // plan ids whose buffer needs fit
+  std::vector<OpTime> last_ops;
 
   void* exch(int rank, int slot, int parity) const;
   uint64_t* flags_of(int rank) const;

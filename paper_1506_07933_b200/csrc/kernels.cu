@@ -94,46 +94,51 @@ struct TmaCfg {
 };
 
 template <typename T, int N, bool ADJ, int LK, bool SPEC = false>
-static cudaError_t launch_tma_tn(const PassParams& p, const TmaPlan& tp, cudaStream_t s) {
+static cudaError_t launch_tma_tn(const PassParams& p, const TmaPlan& tp, int grid_limit, cudaStream_t s) {
   using Cf = TmaCfg<T, N>;
   auto kern = fft_pass_tma_kernel<T, N, Cf::EPREF, Cf::W, ADJ, Cf::STAGES, LK, SPEC>;
-  static int grid_cap[64] = {0};
+  static int occ_of[64] = {0}, sms_of[64] = {0};
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
-  if (!grid_cap[dev]) {
+  if (!occ_of[dev]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM);
     if (e != cudaSuccess) return e;
     int occ = 0, sms = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Cf::THREADS, Cf::SMEM);
     if (e != cudaSuccess) return e;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    grid_cap[dev] = (occ < 1 ? 1 : occ) * sms;
+    sms_of[dev] = sms;
+    occ_of[dev] = occ < 1 ? 1 : occ;
   }
   if (tp.args.ntiles <= 0) return cudaSuccess;
-  const int64_t grid = tp.args.ntiles < grid_cap[dev] ? tp.args.ntiles : grid_cap[dev];
+  // persistent: one wave of resident CTAs on all SMs, or on `grid_limit` SMs
+  // when the caller splits the GPU between two concurrent passes
+  const int sms = grid_limit > 0 && grid_limit < sms_of[dev] ? grid_limit : sms_of[dev];
+  const int64_t cap = (int64_t)occ_of[dev] * sms;
+  const int64_t grid = tp.args.ntiles < cap ? tp.args.ntiles : cap;
   kern<<<(unsigned)grid, Cf::THREADS, Cf::SMEM, s>>>(p, tp.tmap, tp.args);
   count_launch();
   return cudaGetLastError();
 }
 
 template <typename T>
-static cudaError_t launch_tma_prec(int n, const PassParams& p, bool adj, const TmaPlan& tp,
+static cudaError_t launch_tma_prec(int n, const PassParams& p, bool adj, const TmaPlan& tp, int gl,
                                    cudaStream_t s) {
   const int lk = p.in_mode == kInReal ? kR2C : (p.in_mode == kInHermitian ? kC2R : (p.inverse ? kC2CBwd : kC2CFwd));
 #define DFFTB_TMA_CASE(NN)                                                \
   case NN:                                                                \
     if (adj) {                                                            \
-      if (lk == kC2CFwd && p.spec.op) return launch_tma_tn<T, NN, true, kC2CFwd, true>(p, tp, s); \
-      if (lk == kC2CFwd) return launch_tma_tn<T, NN, true, kC2CFwd>(p, tp, s);  \
-      if (lk == kC2CBwd) return launch_tma_tn<T, NN, true, kC2CBwd>(p, tp, s);  \
+      if (lk == kC2CFwd && p.spec.op) return launch_tma_tn<T, NN, true, kC2CFwd, true>(p, tp, gl, s); \
+      if (lk == kC2CFwd) return launch_tma_tn<T, NN, true, kC2CFwd>(p, tp, gl, s);  \
+      if (lk == kC2CBwd) return launch_tma_tn<T, NN, true, kC2CBwd>(p, tp, gl, s);  \
       return cudaErrorInvalidValue;                                       \
     }                                                                     \
     switch (lk) {                                                         \
-      case kC2CFwd: return launch_tma_tn<T, NN, false, kC2CFwd>(p, tp, s);     \
-      case kC2CBwd: return launch_tma_tn<T, NN, false, kC2CBwd>(p, tp, s);     \
-      case kR2C: return launch_tma_tn<T, NN, false, kR2C>(p, tp, s);           \
-      default: return launch_tma_tn<T, NN, false, kC2R>(p, tp, s);             \
+      case kC2CFwd: return launch_tma_tn<T, NN, false, kC2CFwd>(p, tp, gl, s);     \
+      case kC2CBwd: return launch_tma_tn<T, NN, false, kC2CBwd>(p, tp, gl, s);     \
+      case kR2C: return launch_tma_tn<T, NN, false, kR2C>(p, tp, gl, s);           \
+      default: return launch_tma_tn<T, NN, false, kC2R>(p, tp, gl, s);             \
     }
   switch (n) {
     DFFTB_TMA_CASE(8)
@@ -171,141 +176,10 @@ static int tma_w_prec(int n) {
 int tma_tile_w(int prec, int n) { return prec == 8 ? tma_w_prec<double>(n) : tma_w_prec<float>(n); }
 
 
-// ----------------------------------------------- fused two-axis plane pipeline
-
-template <typename T, int N, bool FWD>
-static cudaError_t launch_fused2_tn(const PassParams& pa, const PassParams& pb, const CUtensorMap& tm,
-                                    const Fused2Args& fa, cudaStream_t s) {
-  using Cf = TmaCfg<T, N>;
-  using TL = TmaLayout<T, N, Cf::W>;
-  constexpr int SMEM = 2 * TL::STG + TL::XCH + 16 + 8 * kMaxDest;
-  auto kern = fft_fused2_kernel<T, N, Cf::EPREF, Cf::W, FWD>;
-  static int grid_cap[64] = {0};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
-  if (!grid_cap[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-    if (e != cudaSuccess) return e;
-    int occ = 0, sms = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Cf::THREADS, SMEM);
-    if (e != cudaSuccess) return e;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    grid_cap[dev] = (occ < 1 ? 1 : occ) * sms;  // all CTAs co-resident (dependency waits)
-  }
-  const int64_t items = (int64_t)(fa.P + fa.lag) * 2 * fa.T;
-  const int64_t grid = items < grid_cap[dev] ? items : grid_cap[dev];
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)grid);
-  cfg.blockDim = dim3(Cf::THREADS);
-  cfg.dynamicSmemBytes = SMEM;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  if (fa.persist_bytes > 0) {
-    // the ring persists in L2; everything else streams through
-    attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
-    attr[0].val.accessPolicyWindow.base_ptr = fa.ring;
-    attr[0].val.accessPolicyWindow.num_bytes = fa.persist_bytes;
-    attr[0].val.accessPolicyWindow.hitRatio = 1.0f;
-    attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-    attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-  }
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, pa, pb, tm, fa);
-  count_launch();
-  return e != cudaSuccess ? e : cudaGetLastError();
-}
-
-template <typename T>
-static cudaError_t launch_fused2_prec(int n, bool fwd, const PassParams& pa, const PassParams& pb,
-                                      const CUtensorMap& tm, const Fused2Args& fa, cudaStream_t s) {
-  switch (n) {
-    case 64: return fwd ? launch_fused2_tn<T, 64, true>(pa, pb, tm, fa, s) : launch_fused2_tn<T, 64, false>(pa, pb, tm, fa, s);
-    case 128: return fwd ? launch_fused2_tn<T, 128, true>(pa, pb, tm, fa, s) : launch_fused2_tn<T, 128, false>(pa, pb, tm, fa, s);
-    case 256: return fwd ? launch_fused2_tn<T, 256, true>(pa, pb, tm, fa, s) : launch_fused2_tn<T, 256, false>(pa, pb, tm, fa, s);
-    case 512: return fwd ? launch_fused2_tn<T, 512, true>(pa, pb, tm, fa, s) : launch_fused2_tn<T, 512, false>(pa, pb, tm, fa, s);
-  }
-  return cudaErrorInvalidValue;
-}
-
-bool fused2_supported(int prec, int n) {
-  return (n == 64 || n == 128 || n == 256 || n == 512) && tma_tile_w(prec, n) > 0;
-}
-
-cudaError_t launch_fused2(int prec, int n, bool fwd, const PassParams& pa, const PassParams& pb,
-                          const CUtensorMap& tm, const Fused2Args& fa, cudaStream_t s) {
-  return prec == 8 ? launch_fused2_prec<double>(n, fwd, pa, pb, tm, fa, s)
-                   : launch_fused2_prec<float>(n, fwd, pa, pb, tm, fa, s);
-}
-
-// ------------------------------------------------ pipelined pass pairs
-
-template <typename T, int N, bool ADJ_A, bool ADJ_B, int LK>
-static cudaError_t launch_pipe_tn(const PassParams& pa, const TmaPlan& ta, const PipeArgs& ppa,
-                                  const PassParams& pb, const TmaPlan& tb, const PipeArgs& ppb, double frac_a,
-                                  cudaStream_t s) {
-  using Cf = TmaCfg<T, N>;
-  auto kern = fft_pipe_kernel<T, N, Cf::EPREF, Cf::W, ADJ_A, ADJ_B, Cf::STAGES, LK>;
-  static int grid_cap[64] = {0};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
-  if (!grid_cap[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM);
-    if (e != cudaSuccess) return e;
-    int occ = 0, sms = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Cf::THREADS, Cf::SMEM);
-    if (e != cudaSuccess) return e;
-    if (occ < 1) return cudaErrorInvalidConfiguration;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    grid_cap[dev] = occ * sms;  // every CTA co-resident: the consumer's waits always resolve
-  }
-  const int cap = grid_cap[dev];
-  int na = (int)(frac_a * cap + 0.5);
-  na = na < 1 ? 1 : (na > cap - 1 ? cap - 1 : na);
-  kern<<<(unsigned)cap, Cf::THREADS, Cf::SMEM, s>>>(pa, ta.tmap, ta.args, ppa, pb, tb.tmap, tb.args, ppb, na);
-  count_launch();
-  return cudaGetLastError();
-}
-
-template <typename T, int N>
-static cudaError_t launch_pipe_n(const PassParams& pa, bool adj_a, const TmaPlan& ta, const PipeArgs& ppa,
-                                 const PassParams& pb, bool adj_b, const TmaPlan& tb, const PipeArgs& ppb,
-                                 double frac_a, cudaStream_t s) {
-  const bool bwd = pa.inverse != 0;
-#define DFFTB_PIPE(AA, AB)                                                                            \
-  if (adj_a == AA && adj_b == AB)                                                                     \
-    return bwd ? launch_pipe_tn<T, N, AA, AB, kC2CBwd>(pa, ta, ppa, pb, tb, ppb, frac_a, s)           \
-               : launch_pipe_tn<T, N, AA, AB, kC2CFwd>(pa, ta, ppa, pb, tb, ppb, frac_a, s);
-  DFFTB_PIPE(false, true)
-  DFFTB_PIPE(true, true)
-  DFFTB_PIPE(true, false)
-#undef DFFTB_PIPE
-  return cudaErrorInvalidValue;
-}
-
-bool pipe_supported(int prec, int n) { return (prec == 8 || prec == 4) && (n == 256 || n == 512 || n == 1024); }
-
-cudaError_t launch_pipe(int prec, int n, const PassParams& pa, bool adj_a, const TmaPlan& ta, const PipeArgs& ppa,
-                        const PassParams& pb, bool adj_b, const TmaPlan& tb, const PipeArgs& ppb, double frac_a,
-                        cudaStream_t s) {
-#define DFFTB_PIPE_N(NN)                                                                              \
-  case NN:                                                                                            \
-    return prec == 8 ? launch_pipe_n<double, NN>(pa, adj_a, ta, ppa, pb, adj_b, tb, ppb, frac_a, s)   \
-                     : launch_pipe_n<float, NN>(pa, adj_a, ta, ppa, pb, adj_b, tb, ppb, frac_a, s);
-  switch (n) {
-    DFFTB_PIPE_N(256)
-    DFFTB_PIPE_N(512)
-    DFFTB_PIPE_N(1024)
-  }
-#undef DFFTB_PIPE_N
-  return cudaErrorInvalidValue;
-}
-
-cudaError_t launch_pass_tma(int prec, int n, const PassParams& p, bool adj, const TmaPlan& tp,
+cudaError_t launch_pass_tma(int prec, int n, const PassParams& p, bool adj, const TmaPlan& tp, int grid_limit,
                             cudaStream_t s) {
-  return prec == 8 ? launch_tma_prec<double>(n, p, adj, tp, s) : launch_tma_prec<float>(n, p, adj, tp, s);
+  return prec == 8 ? launch_tma_prec<double>(n, p, adj, tp, grid_limit, s)
+                   : launch_tma_prec<float>(n, p, adj, tp, grid_limit, s);
 }
 
 // ------------------------------------------------------- generic lengths
@@ -337,43 +211,74 @@ cudaError_t launch_pass(int prec, int n, const PassParams& p, bool adj, cudaStre
   return prec == 8 ? launch_prec<double>(n, p, adj, s) : launch_prec<float>(n, p, adj, s);
 }
 
-// ----------------------------------------------------------- group barrier
+// ------------------------------------------------------ cross-GPU sync points
+//
+// Every rank runs the same program, so sync point k of execute e is the same
+// on all ranks.  Rank r's flag page holds one u64 per (sync point, world
+// rank): flags[k * kMaxRanks + q] = the last execute epoch in which rank q
+// reached sync point k with r.  The epoch lives on the device (sync_begin
+// bumps it at the start of every multi-rank program), so programs are
+// replayable (CUDA graphs) without host parameters.  A wait that exceeds the
+// timeout (GPU global timer) raises the context's timeout flag instead of
+// hanging the GPU.
 
-// Cross-GPU barrier over one grid-axis group.  Thread i signals member i
-// (system-scope release store into the member's flag slot for this rank),
-// then waits for member i's flag in the local slot array.  Flags are
-// monotonically increasing epochs, so no reset is ever needed.  A timeout
-// (GPU global timer) turns a dead peer into a reported Deadlock instead of a
-// hung GPU.
-__global__ void group_barrier_kernel(BarrierParams bp) {
-  const int i = threadIdx.x;
-  if (i < bp.nmem && bp.members[i] != bp.me) {
-    __threadfence_system();
-    unsigned long long* dst = bp.peer_flags[i] + bp.me;
-    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(dst), "l"(bp.epoch) : "memory");
-  }
-  if (i < bp.nmem && bp.members[i] != bp.me) {
-    const unsigned long long* src = bp.my_flags + bp.members[i];
-    unsigned long long t0;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-    while (true) {
-      unsigned long long v;
-      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(src) : "memory");
-      if (v >= bp.epoch) break;
-      unsigned long long t1;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-      if (t1 - t0 > bp.timeout_ns) {
-        atomicExch(bp.timeout_flag, 1ull);
-        break;
-      }
-      __nanosleep(100);
-    }
-  }
-  __syncthreads();
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
 }
 
-cudaError_t launch_barrier(const BarrierParams& bp, cudaStream_t s) {
-  group_barrier_kernel<<<1, 32, 0, s>>>(bp);
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// program start: epoch += 1 and the C2R statistics cleared (one thread)
+__global__ void sync_begin_kernel(unsigned long long* epoch, unsigned long long* herm) {
+  if (threadIdx.x == 0) {
+    *epoch += 1;
+    if (herm) {
+      herm[0] = 0;
+      herm[1] = 0;
+    }
+  }
+}
+
+// thread i < nmem serves member i: signal (release store of the epoch into
+// the member's flag page) and/or wait (acquire-spin on my flag for member i)
+__global__ void sync_point_kernel(SyncParams sp) {
+  const int i = threadIdx.x;
+  if (i >= sp.nmem || sp.members[i] == sp.me) return;
+  const unsigned long long e = *sp.epoch;
+  if (sp.signal) {
+    __threadfence_system();
+    unsigned long long* dst = sp.peer_flags[i] + (size_t)sp.slot * kMaxRanksDev + sp.me;
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(dst), "l"(e) : "memory");
+  }
+  if (sp.wait) {
+    const unsigned long long* src = sp.my_flags + (size_t)sp.slot * kMaxRanksDev + sp.members[i];
+    if (ld_acquire_sys(src) >= e) return;
+    if (ld_acquire_sys(sp.timeout_flag) != 0) return;  // this execute already failed
+    const unsigned long long t0 = gtimer();
+    while (ld_acquire_sys(src) < e) {
+      if (gtimer() - t0 > sp.timeout_ns) {
+        atomicExch(sp.timeout_flag, 1ull);
+        break;
+      }
+      __nanosleep(64);
+    }
+  }
+}
+
+cudaError_t launch_sync_begin(unsigned long long* epoch, unsigned long long* herm, cudaStream_t s) {
+  sync_begin_kernel<<<1, 32, 0, s>>>(epoch, herm);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sync_point(const SyncParams& sp, cudaStream_t s) {
+  sync_point_kernel<<<1, 64, 0, s>>>(sp);
   count_launch();
   return cudaGetLastError();
 }

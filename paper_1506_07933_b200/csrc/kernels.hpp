@@ -7,17 +7,21 @@
 #include "fft_generic.cuh"
 #include "fft_pass.cuh"
 #include "fft_pass_tma.cuh"
-#include "fft_fused2.cuh"
 
 namespace dfftb {
 
-struct BarrierParams {
-  unsigned long long* peer_flags[kMaxDest];  // member i's flag array (mapped)
+constexpr int kMaxRanksDev = 64;  // flag-page row length (world ranks)
+constexpr int kSyncSlots = 64;    // sync points per program
+
+struct SyncParams {
+  unsigned long long* peer_flags[kMaxDest];  // member i's flag page (mapped)
   int members[kMaxDest];                     // world ranks of the group
   int nmem;
   int me;                                    // my world rank
-  unsigned long long* my_flags;              // my flag array (indexed by world rank)
-  unsigned long long epoch;
+  int slot;                                  // sync point index in the program
+  int signal, wait;
+  unsigned long long* my_flags;              // my flag page
+  const unsigned long long* epoch;           // device epoch of this context
   unsigned long long timeout_ns;
   unsigned long long* timeout_flag;
 };
@@ -39,18 +43,12 @@ struct TmaPlan {
   TmaArgs args;
 };
 int tma_tile_w(int prec, int n);  // lanes per CTA of the TMA kernel
-bool fused2_supported(int prec, int n);
-cudaError_t launch_fused2(int prec, int n, bool fwd, const PassParams& pa, const PassParams& pb,
-                          const CUtensorMap& tm, const Fused2Args& fa, cudaStream_t s);
-bool pipe_supported(int prec, int n);
-cudaError_t launch_pipe(int prec, int n, const PassParams& pa, bool adj_a, const TmaPlan& ta, const PipeArgs& ppa,
-                        const PassParams& pb, bool adj_b, const TmaPlan& tb, const PipeArgs& ppb, double frac_a,
-                        cudaStream_t s);
-cudaError_t launch_pass_tma(int prec, int n, const PassParams& p, bool adj, const TmaPlan& tp,
+cudaError_t launch_pass_tma(int prec, int n, const PassParams& p, bool adj, const TmaPlan& tp, int grid_limit,
                             cudaStream_t s);
 cudaError_t launch_pass(int prec, int n, const PassParams& p, bool adj, cudaStream_t s);
 cudaError_t launch_generic(int prec, const GenParams& g, cudaStream_t s);
-cudaError_t launch_barrier(const BarrierParams& bp, cudaStream_t s);
+cudaError_t launch_sync_begin(unsigned long long* epoch, unsigned long long* herm, cudaStream_t s);
+cudaError_t launch_sync_point(const SyncParams& sp, cudaStream_t s);
 cudaError_t launch_seeded(int prec, const SeedParams& sp, void* out, cudaStream_t s);
 struct SpectralParams {
   int nd;

@@ -412,6 +412,21 @@ class ExecContext:
         s = stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
         _check(_lib.lib().dfftb_ctx_check(self._h, s))
 
+    def last_ops(self):
+        """Per-op device times of the last execute given `timers`: a list of
+        (kind, stream, length, ms) with kind "local" (FFT pass), "exchange"
+        (FFT pass storing into other ranks' buffers) or "sync"; stream 1 is
+        the overlapped pass on the context's side stream."""
+        L = _lib.lib()
+        n = L.dfftb_ctx_last_ops(self._h, None, None, None, None, 0)
+        k = (ctypes.c_int * max(n, 1))()
+        st = (ctypes.c_int * max(n, 1))()
+        ln = (ctypes.c_int * max(n, 1))()
+        ms = (ctypes.c_double * max(n, 1))()
+        L.dfftb_ctx_last_ops(self._h, k, st, ln, ms, n)
+        names = ("local", "exchange", "sync")
+        return [(names[k[i]], st[i], ln[i], ms[i]) for i in range(n)]
+
 
 def _resolve_device(device) -> torch.device:
     dev = torch.device(device) if device is not None else torch.device("cuda")
@@ -463,15 +478,21 @@ def make_context(plan: Plan, comm=None, rank: Optional[int] = None, device=None)
     return ExecContext(h, my, dev, size)
 
 
-def make_world_contexts(plan: Plan, device=None) -> List[ExecContext]:
-    """All P ranks of the plan emulated on ONE device (test harness for the
-    exchange logic when fewer GPUs than ranks exist); use execute_world."""
-    dev = _resolve_device(device)
+def make_world_contexts(plan: Plan, device=None, devices=None) -> List[ExecContext]:
+    """All P ranks of the plan emulated in THIS process (test harness for the
+    exchange logic when fewer processes or GPUs than ranks exist); use
+    execute_world.  `devices`: rank r lives on devices[r % len(devices)]
+    (exchange stores cross NVLink); default: every rank on `device`."""
     P = plan.nranks()
+    if devices is None:
+        devs = [_resolve_device(device)]
+    else:
+        devs = [_resolve_device(d) for d in devices]
     arr = (ctypes.c_void_p * P)()
-    with torch.cuda.device(dev):
-        _check(_lib.lib().dfftb_world_create(plan._h, dev.index, arr))
-    ctxs = [ExecContext(ctypes.c_void_p(arr[r]), r, dev, P) for r in range(P)]
+    ids = (ctypes.c_int * len(devs))(*[d.index for d in devs])
+    with torch.cuda.device(devs[0]):
+        _check(_lib.lib().dfftb_world_create_devices(plan._h, len(devs), ids, arr))
+    ctxs = [ExecContext(ctypes.c_void_p(arr[r]), r, devs[r % len(devs)], P) for r in range(P)]
     for c in ctxs:
         c._world = ctxs
     return ctxs
@@ -527,7 +548,9 @@ def execute_r2c_c2r_roundtrip(forward: Plan, backward: Plan, x: DistTensor, ctx:
 
 def execute_world(plan: Plan, xs: Sequence[DistTensor], ctxs: Sequence[ExecContext],
                   sync: Optional[bool] = None) -> List[DistTensor]:
-    """Lockstep execution of all ranks of an emulated world on one device."""
+    """Lockstep execution of all ranks of an emulated world (rank r's input
+    and output on its context's device); enqueued on the current stream of
+    rank 0's device."""
     P = plan.nranks()
     if len(xs) != P or len(ctxs) != P:
         raise Error(15, "need one input and one context per rank")
@@ -536,13 +559,13 @@ def execute_world(plan: Plan, xs: Sequence[DistTensor], ctxs: Sequence[ExecConte
         if x.dist != plan.input or x.rank != r:
             raise Error(17, "input layout differs from the plan's")
         outs.append(DistTensor(plan.output, r, torch.empty(
-            plan.output.local_count(r), dtype=plan.dtype_of(plan.output), device=x.data.device)))
+            plan.output.local_count(r), dtype=plan.dtype_of(plan.output), device=ctxs[r].device)))
     if sync is None:
         sync = _needs_sync(plan)
     ins = (ctypes.c_void_p * P)(*[x.data.data_ptr() for x in xs])
     os_ = (ctypes.c_void_p * P)(*[o.data.data_ptr() for o in outs])
     hs = (ctypes.c_void_p * P)(*[c._h.value for c in ctxs])
-    dev = xs[0].data.device
+    dev = ctxs[0].device
     with torch.cuda.device(dev):
         _check(_lib.lib().dfftb_execute_world(plan._h, hs, ins, os_,
                                               torch.cuda.current_stream(dev).cuda_stream,

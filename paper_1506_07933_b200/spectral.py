@@ -110,6 +110,30 @@ class SpectralContext:
         return out
 
 
+def world_forward_op(fwd: Plan, ctxs: Sequence[ExecContext], xs: Sequence[DistTensor], op: int, axis: int = 0,
+                     domain_lengths=None, outs: Optional[Sequence[DistTensor]] = None,
+                     accumulate: bool = False) -> List[DistTensor]:
+    """dfftb_execute_world_spectral: outs[r] (+)= op(forward(x))[r] for every
+    rank of an emulated world (make_world_contexts), the multiplier fused
+    into the forward's last pass.  Test harness for multi-rank spectral
+    operators on fewer GPUs than ranks."""
+    P = fwd.nranks()
+    nd = len(fwd.dims)
+    lens = _lengths(domain_lengths, nd)
+    if outs is None:
+        outs = [DistTensor(fwd.output, r, torch.empty(fwd.output.local_count(r), dtype=fwd.dtype_of(fwd.output),
+                                                      device=ctxs[r].device)) for r in range(P)]
+    ins = (ctypes.c_void_p * P)(*[x.data.data_ptr() for x in xs])
+    os_ = (ctypes.c_void_p * P)(*[o.data.data_ptr() for o in outs])
+    hs = (ctypes.c_void_p * P)(*[c._h.value for c in ctxs])
+    dev = ctxs[0].device
+    with torch.cuda.device(dev):
+        _check(_lib.lib().dfftb_execute_world_spectral(fwd._h, hs, ins, os_, op, axis, lens,
+                                                       1 if accumulate else 0,
+                                                       torch.cuda.current_stream(dev).cuda_stream, 1))
+    return list(outs)
+
+
 def make_spectral_context(dims, grid, domain_lengths=None, precision="f64", comm=None, rank=None,
                           decomp="pencil") -> SpectralContext:
     return SpectralContext(dims, grid, domain_lengths, precision, comm, rank, decomp)

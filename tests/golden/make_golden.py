@@ -6,7 +6,12 @@ plan/execute API by oracle/ref_driver.cpp) on small seeded configurations and
 stores the global input, forward spectrum and backward(forward(x)) round trip
 as raw little-endian arrays next to this script, indexed by golden.json.
 
-Re-run with:  make -C oracle ref && python tests/golden/make_golden.py
+Spectral goldens (SPECTRAL_CASES): the reference's derivative / laplacian /
+inverse_laplacian / divergence (spectral.hpp:131-309) of the seeded field
+through make_spectral_context (ref_driver --spectral), stored as
+<name>.{in,d0..d(n-1),lap,ilap,div}.bin.
+
+Re-run with:  make -C oracle ref && python tests/golden/make_golden.py [--spectral-only]
 """
 import json
 import os
@@ -45,9 +50,40 @@ CASES = [
 ]
 
 
+# spectral operators: name, dims, grid (pencil / general by its length), kind, prec
+SPECTRAL_CASES = [
+    ("spec_c2c_16x8x16_pencil2x2_f64", [16, 8, 16], [2, 2], "c2c", "f64"),
+    ("spec_r2c_16x8x16_pencil2x2_f64", [16, 8, 16], [2, 2], "r2c", "f64"),
+    ("spec_c2c_16x16x16_pencil1x1_f64", [16, 16, 16], [1, 1], "c2c", "f64"),
+    ("spec_r2c_32x16x8_pencil1x1_f32", [32, 16, 8], [1, 1], "r2c", "f32"),
+    ("spec_c2c_8x4x8x8_general2x1x2_f64", [8, 4, 8, 8], [2, 1, 2], "c2c", "f64"),
+    ("spec_r2c_8x8x4x8_general2x2x1_f64", [8, 8, 4, 8], [2, 2, 1], "r2c", "f64"),
+]
+
+
+def spectral(index_path):
+    with open(index_path) as f:
+        idx = json.load(f)
+    out = []
+    for name, dims, grid, kind, prec in SPECTRAL_CASES:
+        prefix = os.path.join(HERE, name)
+        cmd = [REF, "--dims", ",".join(map(str, dims)), "--grid", ",".join(map(str, grid)),
+               "--kind", kind, "--prec", prec, "--seed", "1", "--spectral", "--dump", prefix]
+        subprocess.run(cmd, check=True, capture_output=True, text=True)
+        out.append({"name": name, "dims": dims, "grid": grid, "kind": kind, "prec": prec, "seed": 1,
+                    "decomp": "pencil" if len(grid) == 2 else "general"})
+        print(name)
+    idx["spectral"] = out
+    with open(index_path, "w") as f:
+        json.dump(idx, f, indent=1)
+
+
 def main():
     if not os.path.exists(REF):
         sys.exit("build the reference first: make -C oracle ref")
+    if "--spectral-only" in sys.argv:
+        spectral(os.path.join(HERE, "golden.json"))
+        return
     index = []
     for name, dims, decomp, grid, kind, prec in CASES:
         prefix = os.path.join(HERE, name)
@@ -63,6 +99,7 @@ def main():
     with open(os.path.join(HERE, "golden.json"), "w") as f:
         json.dump({"generator": "tests/golden/make_golden.py via oracle/_ref/dfft_ref",
                    "cases": index}, f, indent=1)
+    spectral(os.path.join(HERE, "golden.json"))
 
 
 if __name__ == "__main__":

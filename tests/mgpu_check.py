@@ -23,7 +23,7 @@ import paper_1506_07933_b200 as D  # noqa: E402
 from gpu_util import make_plan, rel_l2  # noqa: E402
 
 TOL = {"f64": 1e-12, "f32": 1e-5}
-FLAG_DEV = "cpu" if os.environ.get("DFFTB_TEST_OVERSUBSCRIBE") == "1" else "cuda"  # gloo vs nccl
+FLAG_DEV = "cuda"
 
 
 def cases(P):
@@ -76,15 +76,8 @@ def main():
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
-    if os.environ.get("DFFTB_TEST_OVERSUBSCRIBE") == "1":
-        # more ranks than GPUs (e.g. 8 ranks on 4 GPUs): exercises the 8-rank
-        # process / IPC / group logic; two contexts share each GPU by time slicing
-        local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
-    if os.environ.get("DFFTB_TEST_OVERSUBSCRIBE") == "1":
-        dist.init_process_group("gloo")  # NCCL refuses two ranks on one GPU
-    else:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     ok = True
     for decomp, dims, grid, kind, prec in cases(world):
         fwd = make_plan(decomp, dims, grid, kind, "forward", prec)
@@ -110,14 +103,17 @@ def main():
                   f"fwd vs oracle {e_f:.2e}, round trip {e_r:.2e}", flush=True)
         # fused spectral epilogue == execute + spectral_apply, on every rank
         spec_ok = fused_spectral_matches(fwd, ctx, x, rank)
-        # the (opt-in) pipelined pass pairs give bit-identical blocks
-        os.environ["DFFTB_PIPE"] = "1"
+        # a different chunking of the overlapped exchange (PlanOptions
+        # Pipelined, chunks_per_peer = 3) gives bit-identical blocks
+        fwd3 = make_plan(decomp, dims, grid, kind, "forward", prec,
+                         exchange=D.ExchangePath.Pipelined, chunks_per_peer=3)
+        bwd3 = make_plan(decomp, dims, grid, bk, "backward", prec,
+                         exchange=D.ExchangePath.Pipelined, chunks_per_peer=3)
         for _ in range(2):
-            yp = D.execute(fwd, x, ctx)
-            zp = D.execute(bwd, yp, ctx)
+            yp = D.execute(fwd3, x, ctx)
+            zp = D.execute(bwd3, yp, ctx)
         torch.cuda.synchronize()
         ctx.check()
-        del os.environ["DFFTB_PIPE"]
         pipe_ok = bool(torch.equal(yp.data, y.data)) and bool(torch.equal(zp.data, z.data))
         flags = torch.tensor([1 if spec_ok else 0, 1 if pipe_ok else 0], device=FLAG_DEV)
         dist.all_reduce(flags, op=dist.ReduceOp.MIN)
@@ -125,7 +121,7 @@ def main():
             good = bool(flags[0].item() == 1 and flags[1].item() == 1)
             ok = ok and good
             print(f"{'ok  ' if good else 'FAIL'}   fused spectral epilogue {bool(flags[0].item())}, "
-                  f"pipelined pairs bit-identical {bool(flags[1].item())}", flush=True)
+                  f"3-chunk pipelined exchange bit-identical {bool(flags[1].item())}", flush=True)
         ctx.close()
         dist.barrier()
     flag = torch.tensor([1 if ok else 0], device=FLAG_DEV)

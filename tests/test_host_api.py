@@ -188,14 +188,21 @@ def test_gloo_world_size_2_host_path():
 
 
 def test_workspace_bytes():
-    # dfftb_workspace_bytes (host-only): flag page + one exchange buffer per
-    # transpose stage and parity + the work buffer, each sized for the
-    # largest block of the plan family
+    # dfftb_workspace_bytes (host-only): flag page (64 sync points x 64
+    # ranks) + one exchange buffer per transpose stage and parity + the work
+    # buffer, each sized for the largest block of the plan family, + status
+    # words + the per-axis twiddle (and Bluestein) tables
+    flags = 64 * 64 * 8
     p = D.plan_pencil((512, 512, 512), (2, 4), D.TransformKind.C2C, D.Direction.Forward)
     blk = 512 ** 3 * 16 // 8
-    assert D.workspace_bytes(p, 0) == 4096 + 2 * 2 * blk + blk + 64
+    assert D.workspace_bytes(p, 0) == flags + 2 * 2 * blk + blk + 64 + 512 * 16
     g = D.plan_general((8, 8, 16, 16), (1, 1, 1), D.TransformKind.C2C, D.Direction.Forward)
     blk = 8 * 8 * 16 * 16 * 16
-    assert D.workspace_bytes(g, 0) == 4096 + 2 * 3 * blk + blk + 64  # three transposes
+    assert D.workspace_bytes(g, 0) == flags + 2 * 3 * blk + blk + 64 + (8 + 16) * 16  # three transposes
+    # Bluestein length 17: chirp (17) + kernel spectrum (m = 64), fp32 complex
+    b = D.plan_pencil((17, 4, 4), (1, 1), D.TransformKind.C2C, D.Direction.Forward, precision="f32")
+    blk = 17 * 4 * 4 * 8
+    assert D.workspace_bytes(b, 0) == flags + 2 * 2 * ((blk + 255) // 256 * 256) + (blk + 255) // 256 * 256 \
+        + 64 + (17 + 64) * 8 + 4 * 8
     with pytest.raises(D.Error, match="InvalidRank"):
         D.workspace_bytes(p, 8)

@@ -30,18 +30,3 @@ def test_multi_gpu_parity(n):
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     print(r.stdout[-4000:], r.stderr[-4000:])
     assert r.returncode == 0
-
-
-def test_eight_ranks_oversubscribed():
-    """The headline 8-rank grids (pencil 2x4, slab 8) as 8 processes on the
-    GPUs present (two contexts per GPU when there are 4): the 8-rank IPC,
-    group and barrier logic on real separate processes."""
-    g = _ngpus()
-    if g < 2 or g >= 8:
-        pytest.skip("covered by test_multi_gpu_parity[8] or needs 2+ GPUs")
-    env = dict(os.environ, DFFTB_TEST_OVERSUBSCRIBE="1")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=8",
-           "--master-addr", "127.0.0.1", "--master-port", "29518", os.path.join(HERE, "mgpu_check.py")]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env)
-    print(r.stdout[-4000:], r.stderr[-4000:])
-    assert r.returncode == 0

@@ -1,6 +1,6 @@
 #!/bin/bash
 # A/B sweep of environment settings for the N-GPU bench (first arg: N):
-#   bash tools/envsweep_mp.sh 2 "DFFTB_PIPE=0" "DFFTB_PIPE_FRAC=0.5"
+#   bash tools/envsweep_mp.sh 2 "DFFTB_OVERLAP=0" "DFFTB_OVERLAP_FRAC=0.5"
 n=$1; shift
 for setting in "$@"; do
   env $setting timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 \

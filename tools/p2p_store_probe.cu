@@ -197,5 +197,39 @@ int main() {
     printf("split %d/%d SMs: peer half %.3f ms (%.0f GB/s), local half %.3f ms (%.0f GB/s r+w)\n", g, 148 - g, wa,
            bytes / 2 / (wa * 1e-3) / 1e9, wb, bytes / (wb * 1e-3) / 1e9);
   }
+  // copy engine (cudaMemcpyPeerAsync, DMA) and SM pull (remote loads, local
+  // stores), all GPUs at once
+  for (int mode = 0; mode < 2; ++mode) {
+    float worst = 0;
+    for (int rep = 0; rep < 3; ++rep) {
+      std::vector<cudaEvent_t> e0(n), e1(n);
+      for (int d = 0; d < n; ++d) {
+        cudaSetDevice(d);
+        cudaDeviceSynchronize();
+        cudaEventCreate(&e0[d]);
+        cudaEventCreate(&e1[d]);
+      }
+      for (int d = 0; d < n; ++d) {
+        cudaSetDevice(d);
+        cudaEventRecord(e0[d]);
+        if (mode == 0)
+          cudaMemcpyPeerAsync(buf[(d + 1) % n], (d + 1) % n, src[d], d, bytes);
+        else
+          peer_store<<<148 * 4, 512>>>(buf[d], src[(d + 1) % n], elems, 1);
+        cudaEventRecord(e1[d]);
+      }
+      worst = 0;
+      for (int d = 0; d < n; ++d) {
+        cudaSetDevice(d);
+        cudaEventSynchronize(e1[d]);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0[d], e1[d]);
+        worst = ms > worst ? ms : worst;
+      }
+    }
+    printf("%s: %.0f GB/s per GPU (%d GPUs concurrently)\n",
+           mode == 0 ? "copy engine (cudaMemcpyPeerAsync)" : "SM pull (remote loads, local stores)",
+           bytes / (worst * 1e-3) / 1e9, n);
+  }
   return 0;
 }

@@ -71,6 +71,7 @@ struct Knobs {
   double frac = -1.0;         // DFFTB_OVERLAP_FRAC: SM share of the exchange pass (<0: model)
   bool graphs = true;         // DFFTB_GRAPHS: replay cached programs as CUDA graphs
   bool op_times = false;      // DFFTB_OP_TIMES: print per-op device times of timed executes
+  int chain = -1;             // DFFTB_CHAIN: single-rank contiguous-lane chain (-1 auto, 0 off, 1 on)
 };
 
 static const Knobs& knobs() {
@@ -90,6 +91,7 @@ static const Knobs& knobs() {
     if (const char* e = getenv("DFFTB_OVERLAP_FRAC")) k.frac = atof(e);
     k.graphs = flag("DFFTB_GRAPHS", true);
     k.op_times = flag("DFFTB_OP_TIMES", false);
+    if (const char* e = getenv("DFFTB_CHAIN")) k.chain = atoi(e);
     return k;
   }();
   return k;
@@ -554,11 +556,11 @@ static CUtensorMapL2promotion l2_promotion() {
 
 // the whole pass as one launch box
 static void full_box(TmaArgs& a, const PassParams& p, int W) {
-  const int na = p.A * (p.A1 > 1 ? p.A1 : 1);
+  a.na = p.A * (p.A1 > 1 ? p.A1 : 1);
   a.a0 = 0;
   a.bt0 = 0;
   a.nbt = (p.B + W - 1) / W;
-  a.ntiles = (int64_t)na * a.nbt;
+  a.ntiles = (int64_t)a.na * a.nbt;
 }
 
 // Decide whether a pass can use the TMA-prefetch kernel and build its
@@ -685,7 +687,7 @@ static void plan_generic(Op& op, const Ctx& ctx) {
 // One local pass of a 3-D block: axis v of the buffer `in` (extents len,
 // element strides si) into `out` (strides so over the output extents).
 static Op single_pass(const Ctx& ctx, int v, int n, const int64_t* len, const int64_t* si, const void* in,
-                      void* out, const int64_t* so, int fkind, double scale) {
+                      void* out, const int64_t* so, int fkind, double scale, bool inverse = true) {
   int lanes[2], nl = 0;
   for (int a = 0; a < 3; ++a)
     if (a != v) lanes[nl++] = a;
@@ -707,7 +709,7 @@ static Op single_pass(const Ctx& ctx, int v, int n, const int64_t* len, const in
   p.n_out = fkind == DFFTB_R2C ? n / 2 + 1 : n;
   p.in_mode = fkind == DFFTB_R2C ? kInReal : (fkind == DFFTB_C2R ? kInHermitian : kInComplex);
   p.out_real = fkind == DFFTB_C2R;
-  p.inverse = true;
+  p.inverse = inverse;
   p.scale = scale;
   p.tw = is_pow2(n) ? ctx.twiddles.at(n) : nullptr;
   p.herm = ctx.dstat;
@@ -774,9 +776,99 @@ static bool lower_single(const Plan& plan, const Ctx& ctx, const void* d_in, voi
   return true;
 }
 
+// Single-rank 3-D transforms whose strided-lane passes would load narrow
+// TMA rows (long axes: 1024-point fp64 and 2048-point fp32 tiles hold only 4
+// lanes, 64- and 32-byte rows): every pass stores its output with the NEXT
+// pass's transform axis innermost, so every pass after the first loads whole
+// contiguous lanes (bulk copies, any tile width) and only stores are strided.
+// Stores along a lane axis that is not adjacent in the tile use the
+// alpha-fastest tile order, so the CTAs running at one time fill whole output
+// lines in L2 before they are written back.
+//   C2C / R2C:  user [0,1,2] -F2-> [0,2,1] -F1-> [1,2,0] -F0-> user
+//   C2R:        user [0,1,h] -F1-> [1,h,0] -F0-> [0,1,h] -F2(C2R)-> user
+// (the transforms along different axes commute: results agree to rounding).
+static void strides_in_order(const int64_t* len, const int* order, int64_t* st, bool internal, int prec) {
+  int64_t s = 1;
+  for (int idx = 2; idx >= 0; --idx) {
+    const int a = order[idx];
+    st[a] = s;
+    s *= (idx == 2 && internal) ? inner_pad(len[a], prec) : len[a];
+  }
+}
+
+static bool narrow_rows(int prec, int64_t n) {
+  const int W = tma_tile_w(prec, (int)n);
+  return is_pow2(n) && n >= 8 && W > 0 && 2 * W * prec < 128;
+}
+
+static bool lower_chain(const Plan& plan, const Ctx& ctx, const void* d_in, void* d_out, int parity,
+                        std::vector<Op>& prog) {
+  if (plan.nranks() != 1 || plan.input.ndim() != 3 || knobs().chain == 0) return false;
+  int fkinds[3] = {DFFTB_C2C, DFFTB_C2C, DFFTB_C2C};
+  bool backward = false;
+  double scale = 1.0;
+  for (const auto& st : plan.stages) {
+    if (st.type == StageType::Fft) {
+      backward = st.dir == DFFTB_BACKWARD;
+      fkinds[st.axis] = st.fkind;
+    } else if (st.type == StageType::Normalize) {
+      scale = st.factor;
+    }
+  }
+  const bool c2r = fkinds[2] == DFFTB_C2R, r2c = fkinds[2] == DFFTB_R2C;
+  for (auto n : plan.dims)
+    if (!is_pow2(n)) return false;
+  if (knobs().chain < 0) {
+    // auto: only when a strided pass of the default lowering has narrow rows
+    const bool narrow = narrow_rows(ctx.prec, plan.dims[0]) || narrow_rows(ctx.prec, plan.dims[1]);
+    if (!narrow) return false;
+  }
+  const Dist& din = plan.input;
+  const Dist& dout = plan.output;
+  int64_t off[3], lin[3], lout[3];
+  din.extents_of(0, off, lin);
+  dout.extents_of(0, off, lout);
+  for (int a = 0; a < 3; ++a)
+    if (lin[a] <= 0 || lout[a] <= 0) return false;
+  // complex extents (hatted last axis for R2C / C2R) and spatial lengths
+  int64_t lc[3], n[3];
+  for (int a = 0; a < 3; ++a) {
+    lc[a] = c2r ? lin[a] : lout[a];
+    n[a] = plan.dims[a];
+  }
+  const int prec = ctx.prec;
+  void* b1 = ctx.exch(0, 0, parity);
+  void* b2 = ctx.exch(0, 1, parity);
+  static const int U[3] = {0, 1, 2};
+  int64_t s_in[3], s1[3], s2[3], s_out[3];
+  if (!c2r) {
+    static const int O1[3] = {0, 2, 1}, O2[3] = {1, 2, 0};
+    strides_in_order(lin, U, s_in, false, prec);
+    strides_in_order(lc, O1, s1, true, prec);
+    strides_in_order(lc, O2, s2, true, prec);
+    strides_in_order(lout, U, s_out, false, prec);
+    prog.push_back(single_pass(ctx, 2, (int)n[2], lin, s_in, d_in, b1, s1, r2c ? DFFTB_R2C : DFFTB_C2C, 1.0, backward));
+    prog.push_back(single_pass(ctx, 1, (int)n[1], lc, s1, b1, b2, s2, DFFTB_C2C, 1.0, backward));
+    prog.back().tp.args.afast = prog.back().tma ? 1 : 0;  // stores along alpha (x0)
+    prog.push_back(single_pass(ctx, 0, (int)n[0], lc, s2, b2, d_out, s_out, DFFTB_C2C, scale, backward));
+  } else {
+    static const int O1[3] = {1, 2, 0};
+    strides_in_order(lin, U, s_in, false, prec);
+    strides_in_order(lc, O1, s1, true, prec);
+    strides_in_order(lc, U, s2, true, prec);
+    strides_in_order(lout, U, s_out, false, prec);
+    prog.push_back(single_pass(ctx, 1, (int)n[1], lc, s_in, d_in, b1, s1, DFFTB_C2C, 1.0, backward));
+    prog.back().tp.args.afast = prog.back().tma ? 1 : 0;
+    prog.push_back(single_pass(ctx, 0, (int)n[0], lc, s1, b1, b2, s2, DFFTB_C2C, 1.0, backward));
+    prog.push_back(single_pass(ctx, 2, (int)n[2], lc, s2, b2, d_out, s_out, DFFTB_C2R, scale, backward));
+  }
+  return true;
+}
+
 // One rank's program: fused passes and sync points, in stage order.
 static std::vector<Op> lower(const Plan& plan, const Ctx& ctx, const void* d_in, void* d_out, int parity) {
   std::vector<Op> prog;
+  if (lower_chain(plan, ctx, d_in, d_out, parity, prog)) return prog;
   if (lower_single(plan, ctx, d_in, d_out, parity, prog)) return prog;
   const int me = ctx.rank;
   const void* cur = d_in;
@@ -951,15 +1043,16 @@ static TmaArgs chunk_box(const Op& o, int X, int64_t x0, int64_t x1, int W) {
   const int nbt_all = (o.p.B + W - 1) / W;
   if (X == o.ax_a) {
     a.a0 = (int)x0;
+    a.na = (int)(x1 - x0);
     a.bt0 = 0;
     a.nbt = nbt_all;
-    a.ntiles = (x1 - x0) * (int64_t)nbt_all;
   } else {
     a.a0 = 0;
+    a.na = o.p.A;
     a.bt0 = (int)(x0 / W);
     a.nbt = (int)((x1 - x0 + W - 1) / W);
-    a.ntiles = (int64_t)o.p.A * a.nbt;
   }
+  a.ntiles = (int64_t)a.na * a.nbt;
   return a;
 }
 

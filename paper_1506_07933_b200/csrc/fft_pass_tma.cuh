@@ -22,16 +22,32 @@ enum LaneKind : int { kC2CFwd = 0, kC2CBwd = 1, kR2C = 2, kC2R = 3 };
 
 // A launch covers the tile box [a0, a0 + na) x [bt0, bt0 + nbt) of (alpha,
 // beta tile) -- the whole pass, or one chunk of a pipelined exchange.
+// Tiles are numbered beta-tile fastest, or alpha fastest (`afast`: when the
+// pass stores along alpha, concurrent CTAs then fill whole output lines).
 struct TmaArgs {
   int64_t ntiles;  // na * nbt
   int a0, bt0;     // first alpha, first beta tile of the box
-  int nbt;         // beta tiles per alpha row of the box
+  int na, nbt;     // alphas, beta tiles of the box
+  int afast;       // tile order: alpha fastest
   int i_dim;       // tensor-map dimension holding the lane index i (1 or 2)
   int rows;        // box rows per TMA op (ADJ)
   int bulk;        // 1: contiguous cp.async.bulk, 0: tensor map
   int lane_bytes;  // bulk mode: bytes of one stored lane
   int ldgsts;      // strided lanes: per-thread cp.async (16 B) instead of TMA boxes
 };
+
+// tile t of the launch box -> (alpha, beta tile)
+__device__ __forceinline__ void tile_coords(const TmaArgs& ta, int64_t t, int& alpha, int& bt) {
+  if (ta.afast) {
+    const int q = (int)(t / ta.na);
+    alpha = ta.a0 + (int)(t - (int64_t)q * ta.na);
+    bt = ta.bt0 + q;
+  } else {
+    const int ar = (int)(t / ta.nbt);
+    alpha = ta.a0 + ar;
+    bt = ta.bt0 + (int)(t - (int64_t)ar * ta.nbt);
+  }
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -230,9 +246,9 @@ __global__ void __launch_bounds__(W* Sched<N, EPREF>::TPL, DFFTB_TMA_MINB)
 
   // called by every thread; TMA ops are issued by thread 0 only
   auto issue = [&](int64_t t, int s) {
-    const int ar = (int)(t / ta.nbt);
-    const int alpha = ta.a0 + ar;
-    const int beta0 = (ta.bt0 + (int)(t - (int64_t)ar * ta.nbt)) * W;
+    int alpha, beta0;
+    tile_coords(ta, t, alpha, beta0);
+    beta0 *= W;
     unsigned char* dst = stg + s * TL::STG;
     if (ADJ && ta.ldgsts) {
       // very large row strides (e.g. the axis-0 pass) translate one page per
@@ -290,9 +306,9 @@ __global__ void __launch_bounds__(W* Sched<N, EPREF>::TPL, DFFTB_TMA_MINB)
   for (int64_t t = blockIdx.x; t < ta.ntiles; t += gridDim.x, ++k) {
     const int s = k % STAGES;
     mbar_wait(&bars[s], (uint32_t)((k / STAGES) & 1));
-    const int ar = (int)(t / ta.nbt);
-    const int alpha = ta.a0 + ar;
-    const int beta = (ta.bt0 + (int)(t - (int64_t)ar * ta.nbt)) * W + w;
+    int alpha, beta;
+    tile_coords(ta, t, alpha, beta);
+    beta = beta * W + w;
     const unsigned char* st = stg + s * TL::STG;
     C v[SC::E];
     if constexpr (ADJ) {

@@ -307,18 +307,26 @@ def main():
         rt, den = t[0].item(), t[1].item()
     rt_err = math.sqrt(rt / den)
 
-    # per-pass device times (events around every fused pass; separate loop)
+    # per-pass device times: CUDA events around every pass / sync point of 3
+    # more steps (op by op, no graph), TimingBreakdown + ExecContext.last_ops
     tb_f, tb_b = D.TimingBreakdown(), D.TimingBreakdown()
+    ops = []
     for _ in range(3):
         D.execute(fwd, x, ctx, out=y, timers=tb_f)
+        ops += [("fwd",) + o for o in ctx.last_ops()]
         D.execute(bwd, y, ctx, out=z, timers=tb_b)
-    pass_ms = (tb_f.local_fft + tb_f.wire_comm + tb_b.local_fft + tb_b.wire_comm) / 3 * 1e3
-    passes = 6
+        ops += [("bwd",) + o for o in ctx.last_ops()]
+    pass_ms = sum(o[4] for o in ops if o[1] != "sync") / 3  # per step, all passes
+    exch_ms = sum(o[4] for o in ops if o[1] == "exchange") / 3
+    sync_ms = sum(o[4] for o in ops if o[1] == "sync") / 3
+    passes = 6  # logical passes per fwd+inv (chunks of one pass count once)
     avg_pass_ms = max_over_ranks(pass_ms / passes)
     local_elems = fwd.input.local_count(rank)
     alg_bytes = 2 * 16 * local_elems  # one read + one write of the local block per pass
     peak, peak_kind = peaks()
     achieved = alg_bytes / (avg_pass_ms * 1e-3) / 1e9
+    op_list = [{"dir": o[0], "kind": o[1], "side_stream": bool(o[2]), "n": o[3], "ms": round(o[4], 4)}
+               for o in ops[:len(ops) // 3]]
 
     # end-to-end through the public API with host buffers: every step copies
     # its input from pinned host memory, runs fwd+inv and reads the result
@@ -383,11 +391,12 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and os.path.exists(REF_BIN):
         try:
-            rep, p, g = run_reference(0, 1)
+            rep, p, g = run_reference(1, 3)
             cpu = {"value": FLOP_FWDINV / rep["fwdinv_median_s"] / 1e9, "unit": UNIT, "cores": p,
                    "kind": "reference",
-                   "sample": f"one fwd+inv of 512^3 C2C fp64, pencil {g.replace(',', 'x')}, "
-                             f"{p} rank threads ({rep['fwdinv_median_s']:.2f} s)"}
+                   "sample": f"512^3 C2C fp64 fwd+inv, pencil {g.replace(',', 'x')}, {p} rank threads, "
+                             f"median of 3 reps after 1 warm-up (BASELINE.md protocol): "
+                             f"{rep['fwdinv_median_s']:.2f} s per fwd+inv"}
         except Exception as ex:  # reported, not fatal
             cpu = {"error": str(ex)}
 
@@ -403,13 +412,16 @@ def main():
         t_nvl = nvl / (NVL_MEASURED_GBS * 1e9)
         # SURVEY §8(d) convention: nominal 8 TB/s HBM and 900 GB/s NVLink
         t_nominal = max(2 * 6 * 16 * n_loc / 8.0e12, nvl / 900e9)
-        traffic = None
+        traffic, traffic_src = None, None
         if world == 1:
-            try:
-                with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as f:
-                    traffic = json.load(f)["512^3_c2c_f64_grid1x1"]["dram_bytes_per_pass_avg"]
-            except Exception:
-                traffic = None
+            for src in ("profiles/r2/traffic.json", "profiles/r1_traffic.json"):
+                try:
+                    with open(os.path.join(ROOT, src)) as f:
+                        traffic = json.load(f)["512^3_c2c_f64_grid1x1"]["dram_bytes_per_pass_avg"]
+                    traffic_src = src + " (ncu --set full of the bench's passes, per pass)"
+                    break
+                except Exception:
+                    traffic = None
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
             "warmup": W, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
@@ -423,10 +435,10 @@ def main():
             "roundtrip_rel_l2": rt_err,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "traffic_source": "profiles/r1_traffic.json (ncu --set full, per pass)"
-                         if traffic else None,
+                         "traffic_source": traffic_src,
                          "algorithmic_bytes_per_pass": alg_bytes,
-                         "kernel": "fft_pass_tma_kernel (average over the 6 passes per fwd+inv)",
+                         "kernel": "fft_pass_tma_kernel (average over the 6 passes per fwd+inv; "
+                                   "CUDA events around each pass, 3 steps after the timed region)",
                          "peak_source": peak_kind,
                          "step_bound": "nvlink" if t_nvl > t_hbm else "hbm",
                          "step_roofline_ms": 1e3 * max(t_hbm, t_nvl),
@@ -439,8 +451,14 @@ def main():
             "nvlink_counters": nvl_meas,
             "e2e": e2e,
             "cpu_baseline": cpu,
-            "fwd_breakdown_ms": {"local_fft": tb_f.local_fft / 3 * 1e3,
-                                 "fused_exchange": tb_f.wire_comm / 3 * 1e3},
+            # TimingBreakdown (timing.hpp:16-37) of the forward: local_fft =
+            # local passes; wire_comm = exchange passes (FFT + NVLink stores)
+            # + sync points; pack / unpack / staging_copy are fused (0)
+            "fwd_breakdown_ms": {"local_fft": tb_f.local_fft / 3 * 1e3, "wire_comm": tb_f.wire_comm / 3 * 1e3,
+                                 "pack": 0.0, "unpack": 0.0, "staging_copy": 0.0,
+                                 "total": tb_f.total / 3 * 1e3},
+            "step_ops_ms": {"passes": pass_ms, "exchange_passes": exch_ms, "sync_points": sync_ms},
+            "ops_one_step": op_list,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

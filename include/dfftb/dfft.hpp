@@ -8,6 +8,11 @@
 //   * DistTensor buffers live in device memory (`d_data()`); `real` / `cplx`
 //     host vectors are filled on demand with `to_host()`, and
 //     `fill_from_global` / `from_host()` upload.
+//   * execute() mirrors its output to the host vectors only when the
+//     context's `mirror_to_host` is set (default: on, the reference's
+//     host-vector semantics); execute_device() and the spectral operators'
+//     intermediate spectra never leave the GPU, so chains of transforms are
+//     not PCIe-bound.
 //   * make_context takes a Comm that can all-gather bytes (the reference's
 //     transport::Comm plays this role; LocalComm is the single-rank world).
 #pragma once
@@ -283,7 +288,16 @@ struct DistTensor {
   std::vector<T> real;       // host mirrors, filled by to_host()
   std::vector<cx<T>> cplx;
 
+  /// zero block on the device plus zero host mirrors (reference semantics)
   static DistTensor zeros(const Distribution& d, int rank) {
+    DistTensor t = zeros_device(d, rank);
+    const std::size_t n = static_cast<std::size_t>(d.local_count(rank));
+    if (d.element == ElementKind::Real) t.real.assign(n, T(0));
+    else t.cplx.assign(n, cx<T>(0, 0));
+    return t;
+  }
+  /// zero block on the device only (host mirrors empty until to_host())
+  static DistTensor zeros_device(const Distribution& d, int rank) {
     DistTensor t;
     t.dist = d;
     t.rank = rank;
@@ -291,14 +305,15 @@ struct DistTensor {
     const std::size_t esz = d.element == ElementKind::Real ? sizeof(T) : sizeof(cx<T>);
     t.dev = std::make_shared<DeviceBuffer<T>>(n * esz);
     if (n) cuda_check(cudaMemset(t.dev->p, 0, n * esz));
-    if (d.element == ElementKind::Real) t.real.assign(n, T(0));
-    else t.cplx.assign(n, cx<T>(0, 0));
     return t;
   }
   void* d_data() const { return dev ? dev->p : nullptr; }
-  std::size_t local_size() const { return dist.element == ElementKind::Real ? real.size() : cplx.size(); }
+  std::size_t local_size() const { return static_cast<std::size_t>(dist.local_count(rank)); }
   LocalExtents extents() const { return dist.extents_of(rank); }
   void from_host() {
+    const std::size_t n = local_size();
+    if ((dist.element == ElementKind::Real ? real.size() : cplx.size()) != n)
+      throw Error(ErrorCode::CountMismatch, "CountMismatch: host mirror does not hold the local block");
     if (dist.element == ElementKind::Real) {
       if (!real.empty()) cuda_check(cudaMemcpy(dev->p, real.data(), real.size() * sizeof(T), cudaMemcpyHostToDevice));
     } else if (!cplx.empty()) {
@@ -324,6 +339,8 @@ void fill_from_global(DistTensor<T>& t, F&& value_at) {
   const std::size_t nd = t.dist.dims.ndim();
   std::vector<std::int64_t> coord(nd), idx(nd, 0);
   const std::int64_t count = ext.count();
+  if (t.dist.element == ElementKind::Real) t.real.resize(static_cast<std::size_t>(count));
+  else t.cplx.resize(static_cast<std::size_t>(count));
   for (std::int64_t flat = 0; flat < count; ++flat) {
     std::int64_t global = 0;
     for (std::size_t a = 0; a < nd; ++a) {
@@ -374,6 +391,7 @@ struct ExecContext {
   Comm* world = nullptr;
   std::shared_ptr<CtxHandle> ctx;
   cudaStream_t stream = nullptr;
+  bool mirror_to_host = true;  // execute() also fills the output's host vectors
 };
 
 /// make_context (plan.hpp:365-390): collective over comm; device = current CUDA device
@@ -396,23 +414,36 @@ ExecContext make_context(const Plan<T>& plan, Comm& comm) {
   return c;
 }
 
-/// execute (plan.hpp:463-535): returns this rank's output block (device resident)
+/// execute (plan.hpp:463-535) without the host mirror: the output block
+/// stays on the device (to_host() on demand)
 template <class T>
-DistTensor<T> execute(const Plan<T>& plan, const DistTensor<T>& input, ExecContext& ctx,
-                      TimingBreakdown* timers = nullptr) {
+DistTensor<T> execute_device(const Plan<T>& plan, const DistTensor<T>& input, ExecContext& ctx,
+                             TimingBreakdown* timers = nullptr) {
   if (!(input.dist == plan.input))
     throw Error(ErrorCode::LayoutMismatch, "LayoutMismatch: input layout differs from the plan's");
-  DistTensor<T> out = DistTensor<T>::zeros(plan.output, input.rank);
+  DistTensor<T> out = DistTensor<T>::zeros_device(plan.output, input.rank);
   dfftb_timing tc{};
   const int flags = (plan.kind == TransformKind::C2R || plan.options.validate_finite) ? DFFTB_EXEC_SYNC : 0;
   check(dfftb_execute(plan.handle->h, ctx.ctx->h, input.d_data(), out.d_data(), ctx.stream, flags,
                       timers ? &tc : nullptr));
   if (timers) {
     timers->local_fft += tc.local_fft;
+    timers->pack += tc.pack;
+    timers->unpack += tc.unpack;
+    timers->staging_copy += tc.staging_copy;
     timers->wire_comm += tc.wire_comm;
     timers->total += tc.total;
   }
-  out.to_host();
+  return out;
+}
+
+/// execute (plan.hpp:463-535): this rank's output block, on the device and
+/// (ctx.mirror_to_host) in the host vectors
+template <class T>
+DistTensor<T> execute(const Plan<T>& plan, const DistTensor<T>& input, ExecContext& ctx,
+                      TimingBreakdown* timers = nullptr) {
+  DistTensor<T> out = execute_device(plan, input, ctx, timers);
+  if (ctx.mirror_to_host) out.to_host();
   return out;
 }
 
@@ -422,7 +453,7 @@ DistTensor<T> execute_r2c_c2r_roundtrip(const Plan<T>& fwd, const Plan<T>& bwd, 
   if (fwd.kind != TransformKind::R2C || bwd.kind != TransformKind::C2R || !(fwd.dims == bwd.dims) ||
       !(fwd.grid == bwd.grid))
     throw Error(ErrorCode::GridMismatch, "GridMismatch: round trip needs matching R2C/C2R plans");
-  auto spectrum = execute(fwd, in, ctx, timers);
+  auto spectrum = execute_device(fwd, in, ctx, timers);
   return execute(bwd, spectrum, ctx, timers);
 }
 
@@ -518,7 +549,7 @@ DistTensor<T> derivative(SpectralContext<T>& c, const DistTensor<T>& x, int axis
   const bool real = detail::is_real_field(x);
   const Plan<T>& fwd = real ? c.fwd_r2c : c.fwd_c2c;
   const Plan<T>& bwd = real ? c.bwd_c2r : c.bwd_c2c;
-  auto spec = DistTensor<T>::zeros(fwd.output, x.rank);
+  auto spec = DistTensor<T>::zeros_device(fwd.output, x.rank);
   detail::forward_op(c, fwd, x, DFFTB_SPECTRAL_DERIV, axis, spec, false);
   return execute(bwd, spec, c.exec);
 }
@@ -539,7 +570,7 @@ DistTensor<T> divergence(SpectralContext<T>& c, const std::vector<DistTensor<T>>
   const bool real = detail::is_real_field(comps[0]);
   const Plan<T>& fwd = real ? c.fwd_r2c : c.fwd_c2c;
   const Plan<T>& bwd = real ? c.bwd_c2r : c.bwd_c2c;
-  auto acc = DistTensor<T>::zeros(fwd.output, comps[0].rank);
+  auto acc = DistTensor<T>::zeros_device(fwd.output, comps[0].rank);
   for (std::size_t a = 0; a < comps.size(); ++a)
     detail::forward_op(c, fwd, comps[a], DFFTB_SPECTRAL_DERIV, static_cast<int>(a), acc, a > 0);
   return execute(bwd, acc, c.exec);
@@ -551,7 +582,7 @@ DistTensor<T> laplacian(SpectralContext<T>& c, const DistTensor<T>& x) {
   const bool real = detail::is_real_field(x);
   const Plan<T>& fwd = real ? c.fwd_r2c : c.fwd_c2c;
   const Plan<T>& bwd = real ? c.bwd_c2r : c.bwd_c2c;
-  auto spec = DistTensor<T>::zeros(fwd.output, x.rank);
+  auto spec = DistTensor<T>::zeros_device(fwd.output, x.rank);
   detail::forward_op(c, fwd, x, DFFTB_SPECTRAL_LAPLACIAN, 0, spec, false);
   return execute(bwd, spec, c.exec);
 }
@@ -563,7 +594,7 @@ DistTensor<T> inverse_laplacian(SpectralContext<T>& c, const DistTensor<T>& x) {
   const bool real = detail::is_real_field(x);
   const Plan<T>& fwd = real ? c.fwd_r2c : c.fwd_c2c;
   const Plan<T>& bwd = real ? c.bwd_c2r : c.bwd_c2c;
-  auto spec = DistTensor<T>::zeros(fwd.output, x.rank);
+  auto spec = DistTensor<T>::zeros_device(fwd.output, x.rank);
   detail::forward_op(c, fwd, x, DFFTB_SPECTRAL_INV_LAPLACIAN, 0, spec, false);
   return execute(bwd, spec, c.exec);
 }

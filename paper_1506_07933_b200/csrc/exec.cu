@@ -72,6 +72,7 @@ struct Knobs {
   bool graphs = true;         // DFFTB_GRAPHS: replay cached programs as CUDA graphs
   bool op_times = false;      // DFFTB_OP_TIMES: print per-op device times of timed executes
   int chain = -1;             // DFFTB_CHAIN: single-rank contiguous-lane chain (-1 auto, 0 off, 1 on)
+  bool pdl = true;            // DFFTB_PDL: programmatic dependent launch between passes
 };
 
 static const Knobs& knobs() {
@@ -92,6 +93,7 @@ static const Knobs& knobs() {
     k.graphs = flag("DFFTB_GRAPHS", true);
     k.op_times = flag("DFFTB_OP_TIMES", false);
     if (const char* e = getenv("DFFTB_CHAIN")) k.chain = atoi(e);
+    k.pdl = flag("DFFTB_PDL", true);
     return k;
   }();
   return k;
@@ -481,6 +483,7 @@ struct Program {
   bool multi_stream = false;
   int nevents = 0;
   int uses = 0;  // the first run issues directly (kernel attributes set), later runs replay a graph
+  int64_t kernels = 0;  // dfftb kernels one replay of the graph launches
   cudaGraphExec_t graph = nullptr;
   bool graph_failed = false;
 };
@@ -576,6 +579,7 @@ static bool plan_tma(Op& op, int prec) {
   if ((reinterpret_cast<uintptr_t>(p.in) & 15) != 0) return false;
   TmaPlan& tp = op.tp;
   std::memset(&tp, 0, sizeof(tp));
+  tp.pdl = knobs().pdl ? 1 : 0;
   full_box(tp.args, p, W);
   if (p.A1 > 1 && (p.in_sa1 * (p.in_mode == kInReal ? prec : csize)) % 16) return false;
   if (op.adj) {
@@ -630,11 +634,22 @@ static bool plan_tma(Op& op, int prec) {
   // lanes are adjacent rows (row stride in_sb >= lane length: internal
   // buffers pad odd fp32 rows); W rows go in one bulk copy, padding included
   const int64_t lane_bytes = p.in_sb * esize;
-  if (p.in_sb < lane_elems || p.in_sb > n || lane_bytes % 16) return false;
-  if (p.A > 1 && (p.in_sa * esize) % 16) return false;
-  tp.args.bulk = 1;
-  tp.args.lane_bytes = (int)lane_bytes;
-  return true;
+  if (p.in_sb >= lane_elems && p.in_sb <= n && lane_bytes % 16 == 0) {
+    if (p.A > 1 && (p.in_sa * esize) % 16) return false;
+    tp.args.bulk = 1;
+    tp.args.lane_bytes = (int)lane_bytes;
+    return true;
+  }
+  // contiguous lanes that are not adjacent rows: one bulk copy per lane
+  const int64_t lb = lane_elems * esize;
+  if (p.in_sb > n && lb % 16 == 0 && (p.in_sb * esize) % 16 == 0 && (p.A <= 1 || (p.in_sa * esize) % 16 == 0) &&
+      p.A1 <= 1) {
+    tp.args.bulk = 1;
+    tp.args.gather = 1;
+    tp.args.lane_bytes = (int)lb;
+    return true;
+  }
+  return false;
 }
 
 // Cheapest store addressing the destination table allows: one destination,
@@ -687,10 +702,12 @@ static void plan_generic(Op& op, const Ctx& ctx) {
 // One local pass of a 3-D block: axis v of the buffer `in` (extents len,
 // element strides si) into `out` (strides so over the output extents).
 static Op single_pass(const Ctx& ctx, int v, int n, const int64_t* len, const int64_t* si, const void* in,
-                      void* out, const int64_t* so, int fkind, double scale, bool inverse = true) {
+                      void* out, const int64_t* so, int fkind, double scale, bool inverse = true,
+                      int beta_axis = -1) {
   int lanes[2], nl = 0;
   for (int a = 0; a < 3; ++a)
     if (a != v) lanes[nl++] = a;
+  if (beta_axis >= 0 && beta_axis == lanes[0]) std::swap(lanes[0], lanes[1]);
   const int ax_a = lanes[0], ax_b = lanes[1];
   Op op;
   op.v = v;
@@ -776,17 +793,16 @@ static bool lower_single(const Plan& plan, const Ctx& ctx, const void* d_in, voi
   return true;
 }
 
-// Single-rank 3-D transforms whose strided-lane passes would load narrow
-// TMA rows (long axes: 1024-point fp64 and 2048-point fp32 tiles hold only 4
-// lanes, 64- and 32-byte rows): every pass stores its output with the NEXT
-// pass's transform axis innermost, so every pass after the first loads whole
-// contiguous lanes (bulk copies, any tile width) and only stores are strided.
-// Stores along a lane axis that is not adjacent in the tile use the
-// alpha-fastest tile order, so the CTAs running at one time fill whole output
-// lines in L2 before they are written back.
-//   C2C / R2C:  user [0,1,2] -F2-> [0,2,1] -F1-> [1,2,0] -F0-> user
-//   C2R:        user [0,1,h] -F1-> [1,h,0] -F0-> [0,1,h] -F2(C2R)-> user
+// Single-rank 3-D C2C / R2C transforms whose strided-lane passes would load
+// narrow TMA rows (long axes: 1024-point fp64 and 2048-point fp32 tiles hold
+// only 4 lanes, 64- and 32-byte rows): every pass stores its output with the
+// NEXT pass's transform axis innermost, and its tile's adjacent lanes run
+// along that same axis, so every pass loads whole contiguous lanes (bulk
+// copies) and stores contiguous runs of W elements.
+//   user [0,1,2] -F2-> [0,2,1] -F1 (lanes adjacent in x0)-> [1,2,0] -F0-> user
 // (the transforms along different axes commute: results agree to rounding).
+// C2R keeps the default lowering: its Hermitian input is innermost in the
+// user layout, so some pass must read it along a strided axis.
 static void strides_in_order(const int64_t* len, const int* order, int64_t* st, bool internal, int prec) {
   int64_t s = 1;
   for (int idx = 2; idx >= 0; --idx) {
@@ -816,6 +832,7 @@ static bool lower_chain(const Plan& plan, const Ctx& ctx, const void* d_in, void
     }
   }
   const bool c2r = fkinds[2] == DFFTB_C2R, r2c = fkinds[2] == DFFTB_R2C;
+  if (c2r) return false;
   for (auto n : plan.dims)
     if (!is_pow2(n)) return false;
   if (knobs().chain < 0) {
@@ -841,27 +858,16 @@ static bool lower_chain(const Plan& plan, const Ctx& ctx, const void* d_in, void
   void* b2 = ctx.exch(0, 1, parity);
   static const int U[3] = {0, 1, 2};
   int64_t s_in[3], s1[3], s2[3], s_out[3];
-  if (!c2r) {
-    static const int O1[3] = {0, 2, 1}, O2[3] = {1, 2, 0};
-    strides_in_order(lin, U, s_in, false, prec);
-    strides_in_order(lc, O1, s1, true, prec);
-    strides_in_order(lc, O2, s2, true, prec);
-    strides_in_order(lout, U, s_out, false, prec);
-    prog.push_back(single_pass(ctx, 2, (int)n[2], lin, s_in, d_in, b1, s1, r2c ? DFFTB_R2C : DFFTB_C2C, 1.0, backward));
-    prog.push_back(single_pass(ctx, 1, (int)n[1], lc, s1, b1, b2, s2, DFFTB_C2C, 1.0, backward));
-    prog.back().tp.args.afast = prog.back().tma ? 1 : 0;  // stores along alpha (x0)
-    prog.push_back(single_pass(ctx, 0, (int)n[0], lc, s2, b2, d_out, s_out, DFFTB_C2C, scale, backward));
-  } else {
-    static const int O1[3] = {1, 2, 0};
-    strides_in_order(lin, U, s_in, false, prec);
-    strides_in_order(lc, O1, s1, true, prec);
-    strides_in_order(lc, U, s2, true, prec);
-    strides_in_order(lout, U, s_out, false, prec);
-    prog.push_back(single_pass(ctx, 1, (int)n[1], lc, s_in, d_in, b1, s1, DFFTB_C2C, 1.0, backward));
-    prog.back().tp.args.afast = prog.back().tma ? 1 : 0;
-    prog.push_back(single_pass(ctx, 0, (int)n[0], lc, s1, b1, b2, s2, DFFTB_C2C, 1.0, backward));
-    prog.push_back(single_pass(ctx, 2, (int)n[2], lc, s2, b2, d_out, s_out, DFFTB_C2R, scale, backward));
-  }
+  static const int O1[3] = {0, 2, 1}, O2[3] = {1, 2, 0};
+  strides_in_order(lin, U, s_in, false, prec);
+  strides_in_order(lc, O1, s1, true, prec);
+  strides_in_order(lc, O2, s2, true, prec);
+  strides_in_order(lout, U, s_out, false, prec);
+  prog.push_back(single_pass(ctx, 2, (int)n[2], lin, s_in, d_in, b1, s1, r2c ? DFFTB_R2C : DFFTB_C2C, 1.0, backward));
+  // F1: the tile's adjacent lanes run along x0, the output's innermost axis
+  // (one bulk copy per lane in, contiguous runs out)
+  prog.push_back(single_pass(ctx, 1, (int)n[1], lc, s1, b1, b2, s2, DFFTB_C2C, 1.0, backward, 0));
+  prog.push_back(single_pass(ctx, 0, (int)n[0], lc, s2, b2, d_out, s_out, DFFTB_C2C, scale, backward));
   return true;
 }
 
@@ -1282,8 +1288,11 @@ static void run_graph(Ctx& ctx, Program& pr, cudaStream_t s) {
     cudaStream_t cap = static_cast<cudaStream_t>(ctx.capture);
     cudaGraph_t graph = nullptr;
     CUDA_TRY(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+    const uint64_t before = launch_count();
     try {
       issue_program(ctx, pr, cap);
+      pr.kernels = (int64_t)(launch_count() - before);
+      add_launches(-pr.kernels);  // captured, not executed
     } catch (...) {
       cudaStreamEndCapture(cap, &graph);
       if (graph) cudaGraphDestroy(graph);
@@ -1299,8 +1308,12 @@ static void run_graph(Ctx& ctx, Program& pr, cudaStream_t s) {
       pr.graph_failed = true;
     }
   }
-  if (pr.graph) CUDA_TRY(cudaGraphLaunch(pr.graph, s));
-  else issue_program(ctx, pr, s);
+  if (pr.graph) {
+    CUDA_TRY(cudaGraphLaunch(pr.graph, s));
+    add_launches(pr.kernels);
+  } else {
+    issue_program(ctx, pr, s);
+  }
 }
 
 static std::string program_key(const Plan& plan, const void* d_in, const void* d_out, int parity,

@@ -22,31 +22,23 @@ enum LaneKind : int { kC2CFwd = 0, kC2CBwd = 1, kR2C = 2, kC2R = 3 };
 
 // A launch covers the tile box [a0, a0 + na) x [bt0, bt0 + nbt) of (alpha,
 // beta tile) -- the whole pass, or one chunk of a pipelined exchange.
-// Tiles are numbered beta-tile fastest, or alpha fastest (`afast`: when the
-// pass stores along alpha, concurrent CTAs then fill whole output lines).
 struct TmaArgs {
   int64_t ntiles;  // na * nbt
   int a0, bt0;     // first alpha, first beta tile of the box
   int na, nbt;     // alphas, beta tiles of the box
-  int afast;       // tile order: alpha fastest
   int i_dim;       // tensor-map dimension holding the lane index i (1 or 2)
   int rows;        // box rows per TMA op (ADJ)
   int bulk;        // 1: contiguous cp.async.bulk, 0: tensor map
   int lane_bytes;  // bulk mode: bytes of one stored lane
+  int gather;      // bulk mode: the W lanes are in_sb apart (one copy per lane)
   int ldgsts;      // strided lanes: per-thread cp.async (16 B) instead of TMA boxes
 };
 
-// tile t of the launch box -> (alpha, beta tile)
+// tile t of the launch box -> (alpha, beta tile), beta tiles fastest
 __device__ __forceinline__ void tile_coords(const TmaArgs& ta, int64_t t, int& alpha, int& bt) {
-  if (ta.afast) {
-    const int q = (int)(t / ta.na);
-    alpha = ta.a0 + (int)(t - (int64_t)q * ta.na);
-    bt = ta.bt0 + q;
-  } else {
-    const int ar = (int)(t / ta.nbt);
-    alpha = ta.a0 + ar;
-    bt = ta.bt0 + (int)(t - (int64_t)ar * ta.nbt);
-  }
+  const int ar = (int)(t / ta.nbt);
+  alpha = ta.a0 + ar;
+  bt = ta.bt0 + (int)(t - (int64_t)ar * ta.nbt);
 }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -286,7 +278,14 @@ __global__ void __launch_bounds__(W* Sched<N, EPREF>::TPL, DFFTB_TMA_MINB)
       mbar_expect_tx(&bars[s], bytes);
       const unsigned char* src = reinterpret_cast<const unsigned char*>(p.in) +
                                  (in_alpha_off(p, alpha) + (int64_t)beta0 * p.in_sb) * ESIZE;
-      bulk_load(dst, src, bytes, &bars[s]);
+      if (ta.gather) {
+        // lanes are contiguous but not adjacent: one bulk copy per lane
+        for (int ww = 0; ww < nvalid; ++ww)
+          bulk_load(dst + (size_t)ww * ta.lane_bytes, src + (int64_t)ww * p.in_sb * ESIZE, (uint32_t)ta.lane_bytes,
+                    &bars[s]);
+      } else {
+        bulk_load(dst, src, bytes, &bars[s]);
+      }
     }
   };
 
@@ -295,6 +294,11 @@ __global__ void __launch_bounds__(W* Sched<N, EPREF>::TPL, DFFTB_TMA_MINB)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (tid < kMaxDest) sptr[tid] = p.dest[tid].ptr;
+  // Programmatic dependent launch: everything above (barriers, twiddle bases)
+  // overlaps the previous pass's tail; its output is read only after this.
+  // Dependents may launch once every CTA of this grid is resident.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   __syncthreads();
   for (int s = 0; s < STAGES; ++s) {
     const int64_t t = blockIdx.x + (int64_t)s * gridDim.x;

@@ -13,6 +13,7 @@ namespace dfftb {
 static std::atomic<uint64_t> g_launches{0};
 uint64_t launch_count() { return g_launches.load(); }
 void count_launch() { g_launches.fetch_add(1); }
+void add_launches(int64_t n) { g_launches.fetch_add((uint64_t)n); }
 
 // -------------------------------------------------------- pass launchers
 
@@ -117,9 +118,22 @@ static cudaError_t launch_tma_tn(const PassParams& p, const TmaPlan& tp, int gri
   const int sms = grid_limit > 0 && grid_limit < sms_of[dev] ? grid_limit : sms_of[dev];
   const int64_t cap = (int64_t)occ_of[dev] * sms;
   const int64_t grid = tp.args.ntiles < cap ? tp.args.ntiles : cap;
-  kern<<<(unsigned)grid, Cf::THREADS, Cf::SMEM, s>>>(p, tp.tmap, tp.args);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(Cf::THREADS);
+  cfg.dynamicSmemBytes = Cf::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  if (tp.pdl) {
+    // programmatic dependent launch (the kernel waits on griddepcontrol)
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  }
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, p, tp.tmap, tp.args);
   count_launch();
-  return cudaGetLastError();
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 template <typename T>

@@ -41,6 +41,7 @@ bool pass_length_supported(int64_t n);
 struct TmaPlan {
   CUtensorMap tmap;  // tensor-map mode (strided lanes)
   TmaArgs args;
+  int pdl;           // launch with programmatic stream serialization
 };
 int tma_tile_w(int prec, int n);  // lanes per CTA of the TMA kernel
 cudaError_t launch_pass_tma(int prec, int n, const PassParams& p, bool adj, const TmaPlan& tp, int grid_limit,
@@ -63,5 +64,7 @@ cudaError_t launch_spectral(int prec, const SpectralParams& sp, const void* in, 
 cudaError_t launch_nonfinite(int prec, const void* x, int64_t n_reals, unsigned long long* count,
                              cudaStream_t s);
 uint64_t launch_count();
+// kernels a CUDA-graph replay launches are counted at replay, not at capture
+void add_launches(int64_t n);
 
 }  // namespace dfftb

@@ -94,6 +94,9 @@ def read_tensor(dist: Distribution, rank: int, path: str, device=None) -> DistTe
     arr = read_tensor_file(path)
     if tuple(arr.shape) != tuple(dist.dims):
         raise Error(21, "tensor file dims do not match the layout")
+    if dist.element == ElementKind.Real and np.iscomplexobj(arr):
+        # tensor_file.hpp:63-66: never drop imaginary parts silently
+        raise Error(21, "complex tensor file cannot feed a real layout")
     sl = tuple(slice(o, o + n) for o, n in dist.extents_of(rank))
     blk = np.ascontiguousarray(arr[sl])
     plan = dist._plan

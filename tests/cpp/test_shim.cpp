@@ -107,6 +107,13 @@ static void gpu_tests() {
     double err = 0;
     for (const auto& v : y.cplx) err = std::max(err, std::abs(v - cxd(1, 0)));
     CHECK(err < 1e-12);
+    // device-resident chain: no host mirror until asked for
+    ctx.mirror_to_host = false;
+    auto yd = execute(plan, x, ctx);
+    CHECK(yd.cplx.empty() && yd.local_size() == 512);
+    auto yd2 = execute_device(plan, x, ctx);
+    yd2.to_host();
+    CHECK(yd2.cplx.size() == 512 && yd2.cplx[17] == y.cplx[17]);
   }
   {  // test_plan.cpp:367-390 — R2C/C2R round trip is the identity
     const GlobalDims dims{8, 8, 8};

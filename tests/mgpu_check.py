@@ -59,6 +59,41 @@ def fused_spectral_matches(fwd, ctx, x, rank):
     return bool(torch.equal(fused, unf))
 
 
+def validate_keeps_lockstep(rank, world):
+    """A rank whose input fails validate_finite raises ConfigInvalid, but only
+    after issuing its whole program, so the ranks' sync points and exchange
+    buffer parities stay aligned: the next executes are correct everywhere."""
+    dims, grid = [32, 64, 16], [world, 1]
+    fwd = make_plan("pencil", dims, grid, "c2c", "forward", "f64", validate_finite=True)
+    ctx = D.make_context(fwd)
+    x = D.DistTensor.seeded(fwd.input, rank)
+    bad = D.DistTensor(fwd.input, rank, x.data.clone())
+    if rank == 1:
+        bad.data[0] = float("nan")
+    raised = False
+    try:
+        D.execute(fwd, bad, ctx)
+    except D.Error as e:
+        raised = str(e).startswith("ConfigInvalid")
+    good = raised == (rank == 1)
+    for _ in range(3):
+        y = D.execute(fwd, x, ctx)
+    torch.cuda.synchronize()
+    ctx.check()
+    yg = gather_global(fwd.output, y, rank, world)
+    res = torch.tensor([1 if good else 0], device=FLAG_DEV)
+    dist.all_reduce(res, op=dist.ReduceOp.MIN)
+    ok = bool(res.item() == 1)
+    if rank == 0:
+        y_ref, _ = O.execute(O.seeded(dims, True), dims, "pencil", grid, "c2c", "forward")
+        e = rel_l2(yg, y_ref)
+        ok = ok and e <= 1e-12
+        print(f"{'ok  ' if ok else 'FAIL'}   validate_finite on one rank keeps the ranks in lockstep "
+              f"(raised only on rank 1: {good}; next executes vs oracle {e:.2e})", flush=True)
+    ctx.close()
+    return ok
+
+
 def gather_global(dist_, block, rank, world):
     blocks = [None] * world
     dist.all_gather_object(blocks, block.data.cpu().numpy())
@@ -124,6 +159,7 @@ def main():
                   f"3-chunk pipelined exchange bit-identical {bool(flags[1].item())}", flush=True)
         ctx.close()
         dist.barrier()
+    ok = validate_keeps_lockstep(rank, world) and ok
     flag = torch.tensor([1 if ok else 0], device=FLAG_DEV)
     dist.broadcast(flag, 0)
     dist.destroy_process_group()

@@ -46,6 +46,15 @@ def test_dtns_errors(tmp_path):
         IO.read_tensor_file(str(tmp_path / "missing.dtns"))
 
 
+def test_complex_file_cannot_feed_real_layout(tmp_path):
+    # tensor_file.hpp:63-66 (DimMismatch), as the C++ shim's read_tensor
+    p = tmp_path / "c.dtns"
+    IO.write_tensor_file(str(p), np.ones((4, 4, 4), dtype=np.complex128))
+    plan = D.plan_pencil((4, 4, 4), (1, 1), D.TransformKind.R2C, D.Direction.Forward)
+    with pytest.raises(D.Error, match="^DimMismatch: complex tensor file cannot feed a real layout"):
+        IO.read_tensor(plan.input, 0, str(p))
+
+
 def test_report_schema_matches_reference_golden():
     reps = [dict(zip(IO.TIMING_KEYS, [1e-3 * (i + 1)] * 6)) for i in range(3)]
     cfg = {"dims": [8, 8, 8], "grid": [2, 2], "kind": "c2c", "decomp": "pencil", "backend": "b200",

@@ -1,4 +1,5 @@
-"""Per-op times (DFFTB_OP_TIMES) of one fwd+inv of a configuration on one GPU:
+"""Per-op device times (ExecContext.last_ops) of one fwd+inv of a
+configuration on one GPU:
 python tools/op_times_config.py 256,256,256 r2c f64 slab"""
 import os
 import sys
@@ -24,8 +25,12 @@ for _ in range(3):
     y = D.execute(fwd, x, ctx)
     z = D.execute(bwd, y, ctx)
 torch.cuda.synchronize()
-os.environ["DFFTB_OP_TIMES"] = "1"
-tb = D.TimingBreakdown()
-y = D.execute(fwd, x, ctx, timers=tb)
-z = D.execute(bwd, y, ctx, timers=tb)
-print("total ms", tb.total * 1e3)
+for name in ("fwd", "bwd"):
+    tb = D.TimingBreakdown()
+    if name == "fwd":
+        y = D.execute(fwd, x, ctx, timers=tb)
+    else:
+        z = D.execute(bwd, y, ctx, timers=tb)
+    print(f"{name} total {tb.total * 1e3:.3f} ms")
+    for kind, stream, n, ms in ctx.last_ops():
+        print(f"  {kind:8s} n={n:5d} {ms:.3f} ms")

@@ -66,13 +66,14 @@ struct Knobs {
   bool tma = true;            // DFFTB_NO_TMA=1 disables the TMA pass kernel
   int l2promo = 3;            // DFFTB_L2PROMO: tensor-map L2 promotion 0/64/128/256 B
   bool unaligned_ldgsts = true;  // DFFTB_UNALIGNED_LDGSTS: cp.async loader for odd fp32 rows
-  bool overlap = true;        // DFFTB_OVERLAP: pipelined exchange/local pass pairs
+  int overlap = -1;           // DFFTB_OVERLAP: pipelined exchange/local pass pairs (-1: plans with
+                              // ExchangePath::Pipelined only, 0 never, 1 every multi-rank plan)
   int chunks = 4;             // DFFTB_OVERLAP_CHUNKS: chunks per pipelined pair
   double frac = -1.0;         // DFFTB_OVERLAP_FRAC: SM share of the exchange pass (<0: model)
   bool graphs = true;         // DFFTB_GRAPHS: replay cached programs as CUDA graphs
   bool op_times = false;      // DFFTB_OP_TIMES: print per-op device times of timed executes
-  int chain = -1;             // DFFTB_CHAIN: single-rank contiguous-lane chain (-1 auto, 0 off, 1 on)
   bool pdl = true;            // DFFTB_PDL: programmatic dependent launch between passes
+  bool cl2 = true;            // DFFTB_CL2: 2-CTA cluster pass for long strided lanes
 };
 
 static const Knobs& knobs() {
@@ -87,13 +88,13 @@ static const Knobs& knobs() {
     k.tma = !flag("DFFTB_NO_TMA", false);
     if (const char* e = getenv("DFFTB_L2PROMO")) k.l2promo = atoi(e);
     k.unaligned_ldgsts = flag("DFFTB_UNALIGNED_LDGSTS", true);
-    k.overlap = flag("DFFTB_OVERLAP", true);
+    if (const char* e = getenv("DFFTB_OVERLAP")) k.overlap = atoi(e);
     if (const char* e = getenv("DFFTB_OVERLAP_CHUNKS")) k.chunks = std::max(1, std::min(16, atoi(e)));
     if (const char* e = getenv("DFFTB_OVERLAP_FRAC")) k.frac = atof(e);
     k.graphs = flag("DFFTB_GRAPHS", true);
     k.op_times = flag("DFFTB_OP_TIMES", false);
-    if (const char* e = getenv("DFFTB_CHAIN")) k.chain = atoi(e);
     k.pdl = flag("DFFTB_PDL", true);
+    k.cl2 = flag("DFFTB_CL2", true);
     return k;
   }();
   return k;
@@ -286,8 +287,13 @@ static size_t table_bytes(const Plan& plan) {
   for (auto n : plan.dims) {
     if (std::find(seen.begin(), seen.end(), n) != seen.end()) continue;
     seen.push_back(n);
-    if (is_pow2(n)) t += (size_t)n * 2 * plan.prec;
-    else if (!is_smooth(n)) t += (size_t)(n + bluestein_m(n)) * 2 * plan.prec;
+    if (is_pow2(n)) {
+      t += (size_t)n * 2 * plan.prec;
+      const bool half_seen = std::find(plan.dims.begin(), plan.dims.end(), n / 2) != plan.dims.end();
+      if (cl2_supported(plan.prec, (int)n) && !half_seen) t += (size_t)(n / 2) * 2 * plan.prec;
+    } else if (!is_smooth(n)) {
+      t += (size_t)(n + bluestein_m(n)) * 2 * plan.prec;
+    }
   }
   return t;
 }
@@ -327,10 +333,16 @@ Ctx* ctx_create(const Plan& plan, int rank, int device) {
   CUDA_TRY(cudaMemset(ctx->dstat, 0, kStatWords * sizeof(unsigned long long)));
   // twiddle tables w[m] = exp(-2 pi i m / n) in double, cast to T
   // (TwiddleTable, kernels.hpp:66-98); forward only: backward is conj(F(conj x))
+  std::vector<int> tables;
   for (auto n64 : plan.dims) {
     const int n = (int)n64;
     if (!is_pow2(n) && !is_smooth(n) && !ctx->bluestein.count(n)) ctx->bluestein[n] = bluestein_tables(n, plan.prec);
-    if (!is_pow2(n) || ctx->twiddles.count(n)) continue;
+    if (!is_pow2(n)) continue;
+    tables.push_back(n);
+    if (cl2_supported(plan.prec, n)) tables.push_back(n / 2);  // the 2-CTA cluster pass's stages
+  }
+  for (int n : tables) {
+    if (ctx->twiddles.count(n)) continue;
     std::vector<std::complex<double>> w(n);
     for (int m = 0; m < n; ++m) {
       const double a = -2.0 * M_PI * (double)m / (double)n;
@@ -559,6 +571,7 @@ static CUtensorMapL2promotion l2_promotion() {
 
 // the whole pass as one launch box
 static void full_box(TmaArgs& a, const PassParams& p, int W) {
+  a.W = W;
   a.na = p.A * (p.A1 > 1 ? p.A1 : 1);
   a.a0 = 0;
   a.bt0 = 0;
@@ -573,8 +586,13 @@ static bool plan_tma(Op& op, int prec) {
   const PassParams& p = op.p;
   const int n = op.n;
   if (!knobs().tma || n < 8 || (int64_t)p.A * p.B == 0) return false;
-  const int W = tma_tile_w(prec, n);
+  int W = tma_tile_w(prec, n);
   if (W <= 0) return false;
+  // long strided C2C lanes whose one-CTA tile is narrower than a 128-byte
+  // row: the 2-CTA cluster pass (half of every lane per CTA, twice the lanes)
+  const bool cl2 = knobs().cl2 && op.adj && p.in_mode == kInComplex && !p.out_real && p.A1 <= 1 &&
+                   p.spec.op == 0 && 2 * W * prec < 128 && cl2_supported(prec, n) && op.p.tw2 != nullptr;
+  if (cl2) W = tma_tile_w(prec, n / 2);
   const int csize = 2 * prec;
   if ((reinterpret_cast<uintptr_t>(p.in) & 15) != 0) return false;
   TmaPlan& tp = op.tp;
@@ -591,6 +609,10 @@ static bool plan_tma(Op& op, int prec) {
     if (si % 16 || sa % 16) {
       // rows a tensor map cannot describe (fp32 C2R user blocks: 129-bin
       // rows of 1032 bytes): per-thread 8-byte cp.async into the same tile
+      if (cl2) {
+        W = tma_tile_w(prec, n);
+        full_box(tp.args, p, W);
+      }
       if (csize != 8 || (reinterpret_cast<uintptr_t>(p.in) & 7) || !knobs().unaligned_ldgsts) return false;
       tp.args.bulk = 0;
       tp.args.ldgsts = 1;
@@ -598,7 +620,8 @@ static bool plan_tma(Op& op, int prec) {
     }
     auto enc = tensor_map_encoder();
     if (!enc) return false;
-    const int rows = n < 256 ? n : 256;
+    const int span = cl2 ? n / 2 : n;  // rows one CTA stages
+    const int rows = span < 256 ? span : 256;
     cuuint64_t gdim[3];
     cuuint64_t gstride[2];
     cuuint32_t box[3], estr[3] = {1, 1, 1};
@@ -627,6 +650,7 @@ static bool plan_tma(Op& op, int prec) {
     if (r != CUDA_SUCCESS) return false;
     tp.args.rows = rows;
     tp.args.bulk = 0;
+    tp.args.cl2 = cl2 ? 1 : 0;
     return true;
   }
   const int64_t lane_elems = p.in_mode == kInHermitian ? n / 2 + 1 : n;
@@ -638,15 +662,6 @@ static bool plan_tma(Op& op, int prec) {
     if (p.A > 1 && (p.in_sa * esize) % 16) return false;
     tp.args.bulk = 1;
     tp.args.lane_bytes = (int)lane_bytes;
-    return true;
-  }
-  // contiguous lanes that are not adjacent rows: one bulk copy per lane
-  const int64_t lb = lane_elems * esize;
-  if (p.in_sb > n && lb % 16 == 0 && (p.in_sb * esize) % 16 == 0 && (p.A <= 1 || (p.in_sa * esize) % 16 == 0) &&
-      p.A1 <= 1) {
-    tp.args.bulk = 1;
-    tp.args.gather = 1;
-    tp.args.lane_bytes = (int)lb;
     return true;
   }
   return false;
@@ -676,6 +691,12 @@ static void set_store_mode(PassParams& p) {
 }
 
 // Non-power-of-two lengths run the generic mixed-radix / Bluestein kernel
+// the 2-CTA cluster pass runs NH = n/2 point Stockham stages (tw = the
+// n/2-point table) after a cross-CTA radix-2 step (tw2 = the n-point table)
+static void plan_twiddles(Op& op, const Ctx& ctx) {
+  if (op.tma && op.tp.args.cl2) op.p.tw = ctx.twiddles.at(op.n / 2);
+}
+
 static void plan_generic(Op& op, const Ctx& ctx) {
   if (is_pow2(op.n)) return;
   op.tma = false;
@@ -702,12 +723,10 @@ static void plan_generic(Op& op, const Ctx& ctx) {
 // One local pass of a 3-D block: axis v of the buffer `in` (extents len,
 // element strides si) into `out` (strides so over the output extents).
 static Op single_pass(const Ctx& ctx, int v, int n, const int64_t* len, const int64_t* si, const void* in,
-                      void* out, const int64_t* so, int fkind, double scale, bool inverse = true,
-                      int beta_axis = -1) {
+                      void* out, const int64_t* so, int fkind, double scale) {
   int lanes[2], nl = 0;
   for (int a = 0; a < 3; ++a)
     if (a != v) lanes[nl++] = a;
-  if (beta_axis >= 0 && beta_axis == lanes[0]) std::swap(lanes[0], lanes[1]);
   const int ax_a = lanes[0], ax_b = lanes[1];
   Op op;
   op.v = v;
@@ -726,9 +745,10 @@ static Op single_pass(const Ctx& ctx, int v, int n, const int64_t* len, const in
   p.n_out = fkind == DFFTB_R2C ? n / 2 + 1 : n;
   p.in_mode = fkind == DFFTB_R2C ? kInReal : (fkind == DFFTB_C2R ? kInHermitian : kInComplex);
   p.out_real = fkind == DFFTB_C2R;
-  p.inverse = inverse;
+  p.inverse = true;
   p.scale = scale;
   p.tw = is_pow2(n) ? ctx.twiddles.at(n) : nullptr;
+  p.tw2 = is_pow2(n) && n >= 16 && ctx.twiddles.count(n / 2) ? p.tw : nullptr;
   p.herm = ctx.dstat;
   op.adj = p.in_si != 1;
   p.ndest = 1;
@@ -743,6 +763,7 @@ static Op single_pass(const Ctx& ctx, int v, int n, const int64_t* len, const in
   op.tma = false;
   set_store_mode(p);
   op.tma = plan_tma(op, ctx.prec);
+  plan_twiddles(op, ctx);
   plan_generic(op, ctx);
   return op;
 }
@@ -793,88 +814,9 @@ static bool lower_single(const Plan& plan, const Ctx& ctx, const void* d_in, voi
   return true;
 }
 
-// Single-rank 3-D C2C / R2C transforms whose strided-lane passes would load
-// narrow TMA rows (long axes: 1024-point fp64 and 2048-point fp32 tiles hold
-// only 4 lanes, 64- and 32-byte rows): every pass stores its output with the
-// NEXT pass's transform axis innermost, and its tile's adjacent lanes run
-// along that same axis, so every pass loads whole contiguous lanes (bulk
-// copies) and stores contiguous runs of W elements.
-//   user [0,1,2] -F2-> [0,2,1] -F1 (lanes adjacent in x0)-> [1,2,0] -F0-> user
-// (the transforms along different axes commute: results agree to rounding).
-// C2R keeps the default lowering: its Hermitian input is innermost in the
-// user layout, so some pass must read it along a strided axis.
-static void strides_in_order(const int64_t* len, const int* order, int64_t* st, bool internal, int prec) {
-  int64_t s = 1;
-  for (int idx = 2; idx >= 0; --idx) {
-    const int a = order[idx];
-    st[a] = s;
-    s *= (idx == 2 && internal) ? inner_pad(len[a], prec) : len[a];
-  }
-}
-
-static bool narrow_rows(int prec, int64_t n) {
-  const int W = tma_tile_w(prec, (int)n);
-  return is_pow2(n) && n >= 8 && W > 0 && 2 * W * prec < 128;
-}
-
-static bool lower_chain(const Plan& plan, const Ctx& ctx, const void* d_in, void* d_out, int parity,
-                        std::vector<Op>& prog) {
-  if (plan.nranks() != 1 || plan.input.ndim() != 3 || knobs().chain == 0) return false;
-  int fkinds[3] = {DFFTB_C2C, DFFTB_C2C, DFFTB_C2C};
-  bool backward = false;
-  double scale = 1.0;
-  for (const auto& st : plan.stages) {
-    if (st.type == StageType::Fft) {
-      backward = st.dir == DFFTB_BACKWARD;
-      fkinds[st.axis] = st.fkind;
-    } else if (st.type == StageType::Normalize) {
-      scale = st.factor;
-    }
-  }
-  const bool c2r = fkinds[2] == DFFTB_C2R, r2c = fkinds[2] == DFFTB_R2C;
-  if (c2r) return false;
-  for (auto n : plan.dims)
-    if (!is_pow2(n)) return false;
-  if (knobs().chain < 0) {
-    // auto: only when a strided pass of the default lowering has narrow rows
-    const bool narrow = narrow_rows(ctx.prec, plan.dims[0]) || narrow_rows(ctx.prec, plan.dims[1]);
-    if (!narrow) return false;
-  }
-  const Dist& din = plan.input;
-  const Dist& dout = plan.output;
-  int64_t off[3], lin[3], lout[3];
-  din.extents_of(0, off, lin);
-  dout.extents_of(0, off, lout);
-  for (int a = 0; a < 3; ++a)
-    if (lin[a] <= 0 || lout[a] <= 0) return false;
-  // complex extents (hatted last axis for R2C / C2R) and spatial lengths
-  int64_t lc[3], n[3];
-  for (int a = 0; a < 3; ++a) {
-    lc[a] = c2r ? lin[a] : lout[a];
-    n[a] = plan.dims[a];
-  }
-  const int prec = ctx.prec;
-  void* b1 = ctx.exch(0, 0, parity);
-  void* b2 = ctx.exch(0, 1, parity);
-  static const int U[3] = {0, 1, 2};
-  int64_t s_in[3], s1[3], s2[3], s_out[3];
-  static const int O1[3] = {0, 2, 1}, O2[3] = {1, 2, 0};
-  strides_in_order(lin, U, s_in, false, prec);
-  strides_in_order(lc, O1, s1, true, prec);
-  strides_in_order(lc, O2, s2, true, prec);
-  strides_in_order(lout, U, s_out, false, prec);
-  prog.push_back(single_pass(ctx, 2, (int)n[2], lin, s_in, d_in, b1, s1, r2c ? DFFTB_R2C : DFFTB_C2C, 1.0, backward));
-  // F1: the tile's adjacent lanes run along x0, the output's innermost axis
-  // (one bulk copy per lane in, contiguous runs out)
-  prog.push_back(single_pass(ctx, 1, (int)n[1], lc, s1, b1, b2, s2, DFFTB_C2C, 1.0, backward, 0));
-  prog.push_back(single_pass(ctx, 0, (int)n[0], lc, s2, b2, d_out, s_out, DFFTB_C2C, scale, backward));
-  return true;
-}
-
 // One rank's program: fused passes and sync points, in stage order.
 static std::vector<Op> lower(const Plan& plan, const Ctx& ctx, const void* d_in, void* d_out, int parity) {
   std::vector<Op> prog;
-  if (lower_chain(plan, ctx, d_in, d_out, parity, prog)) return prog;
   if (lower_single(plan, ctx, d_in, d_out, parity, prog)) return prog;
   const int me = ctx.rank;
   const void* cur = d_in;
@@ -929,6 +871,7 @@ static std::vector<Op> lower(const Plan& plan, const Ctx& ctx, const void* d_in,
     p.inverse = st.dir == DFFTB_BACKWARD;
     p.scale = nm ? nm->factor : 1.0;
     p.tw = is_pow2(n) ? ctx.twiddles.at(n) : nullptr;
+    p.tw2 = is_pow2(n) && n >= 16 && ctx.twiddles.count(n / 2) ? p.tw : nullptr;
     p.herm = ctx.dstat;
     op.adj = p.in_si != 1;
     if (lenb[v] == 0 && st.fkind != DFFTB_C2R) p.A = 0;
@@ -959,6 +902,7 @@ static std::vector<Op> lower(const Plan& plan, const Ctx& ctx, const void* d_in,
       }
       set_store_mode(p);
       op.tma = plan_tma(op, ctx.prec);
+      plan_twiddles(op, ctx);
       plan_generic(op, ctx);
       prog.push_back(op);
       if (op.remote) {
@@ -990,6 +934,7 @@ static std::vector<Op> lower(const Plan& plan, const Ctx& ctx, const void* d_in,
       d.sk = so[v];
       set_store_mode(p);
       op.tma = plan_tma(op, ctx.prec);
+      plan_twiddles(op, ctx);
       plan_generic(op, ctx);
       prog.push_back(op);
       cur = out;
@@ -1063,10 +1008,10 @@ static TmaArgs chunk_box(const Op& o, int X, int64_t x0, int64_t x1, int W) {
 }
 
 static void overlap_pairs(std::vector<Op>& prog, const Plan& plan, const Ctx& ctx, int& nevents) {
-  if (!knobs().overlap || ctx.world_mode || ctx.nranks < 2) return;
+  const bool pipelined = plan.options.exchange == DFFTB_EXCHANGE_PIPELINED;
+  if (knobs().overlap == 0 || (knobs().overlap < 0 && !pipelined) || ctx.world_mode || ctx.nranks < 2) return;
   int C = knobs().chunks;
-  if (plan.options.exchange == DFFTB_EXCHANGE_PIPELINED && plan.options.chunks_per_peer > 1)
-    C = std::min(16, plan.options.chunks_per_peer);
+  if (pipelined && plan.options.chunks_per_peer > 1) C = std::min(16, plan.options.chunks_per_peer);
   if (C < 2) return;
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx.device);
@@ -1095,7 +1040,7 @@ static void overlap_pairs(std::vector<Op>& prog, const Plan& plan, const Ctx& ct
         ok = ok && o[X] == offQ[X] && l[X] == lenQ[X];
       }
     }
-    const int WP = tma_tile_w(ctx.prec, P.n), WQ = tma_tile_w(ctx.prec, Q.n);
+    const int WP = P.tp.args.W, WQ = Q.tp.args.W;
     const int64_t Xe = ok ? lenQ[X] : 0;
     // chunk length: a whole number of tiles on the beta axis of either pass
     int64_t unit = 1;
@@ -1181,10 +1126,10 @@ static bool plan_has_c2r(const Plan& plan) {
 }
 
 static std::shared_ptr<Program> build_program(const Plan& plan, Ctx& ctx, const void* d_in, void* d_out,
-                                              int parity) {
+                                              int parity, bool allow_overlap = true) {
   auto pr = std::make_shared<Program>();
   std::vector<Op> ops = lower(plan, ctx, d_in, d_out, parity);
-  overlap_pairs(ops, plan, ctx, pr->nevents);
+  if (allow_overlap) overlap_pairs(ops, plan, ctx, pr->nevents);
   assign_slots(ops);
   pr->c2r = plan_has_c2r(plan);
   bool has_sync = false;
@@ -1659,7 +1604,8 @@ static Program& spectral_program(const Plan& plan, Ctx& ctx, const void* d_in, v
   auto it = ctx.programs.find(key);
   if (it != ctx.programs.end()) return *it->second;
   if (ctx.programs.size() >= kMaxCachedPrograms) drop_programs(ctx);
-  auto pr = build_program(plan, ctx, d_in, d_out, parity);
+  // the epilogue goes on ONE launch of the last pass: no chunked overlap
+  auto pr = build_program(plan, ctx, d_in, d_out, parity, false);
   Op* last = nullptr;
   for (auto& o : pr->ops)
     if (o.kind == OpKind::Pass) last = &o;

@@ -1,0 +1,15 @@
+// f32 instantiations of the pass launchers (kernels_launch.cuh).
+#include "kernels_launch.cuh"
+
+namespace dfftb {
+
+cudaError_t launch_pass_f32(int n, const PassParams& p, bool adj, cudaStream_t s) {
+  return launch_prec<float>(n, p, adj, s);
+}
+cudaError_t launch_pass_tma_f32(int n, const PassParams& p, bool adj, const TmaPlan& tp, int grid_limit,
+                                 cudaStream_t s) {
+  return launch_tma_prec<float>(n, p, adj, tp, grid_limit, s);
+}
+int tma_tile_w_f32(int n) { return tma_w_prec<float>(n); }
+
+}  // namespace dfftb

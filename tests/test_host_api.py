@@ -191,11 +191,15 @@ def test_workspace_bytes():
     # dfftb_workspace_bytes (host-only): flag page (64 sync points x 64
     # ranks) + one exchange buffer per transpose stage and parity + the work
     # buffer, each sized for the largest block of the plan family, + status
-    # words + the per-axis twiddle (and Bluestein) tables
+    # words + the per-axis twiddle (and Bluestein) tables (+ the half-length
+    # table of axes >= 1024, for the 2-CTA cluster pass)
     flags = 64 * 64 * 8
     p = D.plan_pencil((512, 512, 512), (2, 4), D.TransformKind.C2C, D.Direction.Forward)
     blk = 512 ** 3 * 16 // 8
     assert D.workspace_bytes(p, 0) == flags + 2 * 2 * blk + blk + 64 + 512 * 16
+    q = D.plan_pencil((1024, 64, 64), (2, 4), D.TransformKind.C2C, D.Direction.Forward)
+    blk = 1024 * 64 * 64 * 16 // 8
+    assert D.workspace_bytes(q, 0) == flags + 2 * 2 * blk + blk + 64 + (1024 + 512 + 64) * 16
     g = D.plan_general((8, 8, 16, 16), (1, 1, 1), D.TransformKind.C2C, D.Direction.Forward)
     blk = 8 * 8 * 16 * 16 * 16
     assert D.workspace_bytes(g, 0) == flags + 2 * 3 * blk + blk + 64 + (8 + 16) * 16  # three transposes

@@ -73,7 +73,7 @@ struct Knobs {
   bool graphs = true;         // DFFTB_GRAPHS: replay cached programs as CUDA graphs
   bool op_times = false;      // DFFTB_OP_TIMES: print per-op device times of timed executes
   bool pdl = true;            // DFFTB_PDL: programmatic dependent launch between passes
-  bool cl2 = true;            // DFFTB_CL2: 2-CTA cluster pass for long strided lanes
+  bool cl2 = false;           // DFFTB_CL2: 2-CTA cluster pass for long strided lanes (opt-in: measured slower)
 };
 
 static const Knobs& knobs() {
@@ -94,7 +94,7 @@ static const Knobs& knobs() {
     k.graphs = flag("DFFTB_GRAPHS", true);
     k.op_times = flag("DFFTB_OP_TIMES", false);
     k.pdl = flag("DFFTB_PDL", true);
-    k.cl2 = flag("DFFTB_CL2", true);
+    k.cl2 = flag("DFFTB_CL2", false);
     return k;
   }();
   return k;
@@ -103,7 +103,8 @@ static const Knobs& knobs() {
 void* Ctx::exch(int r, int slot, int parity) const {
   if (slot < 0 || slot >= exch_slots) raise(DFFTB_ArenaExhausted, "exchange slot out of range");
   char* base = static_cast<char*>(peer_region[r]);
-  return base + flags_bytes + (size_t)(2 * slot + parity) * exch_bytes;
+  if (parities == 1) parity = 0;
+  return base + flags_bytes + (size_t)(parities * slot + parity) * exch_bytes;
 }
 
 uint64_t* Ctx::flags_of(int r) const { return static_cast<uint64_t*>(peer_region[r]); }
@@ -179,6 +180,26 @@ static int family_exch_slots(const Plan& plan) {
     m = std::max(m, t);
   }
   return m;
+}
+
+// Execute parities of the exchange buffers: two when peers may still read
+// one buffer while this rank writes the next execute's data, one for a
+// single rank (stream order already separates its executes).
+static int family_parities(const Plan& plan) { return plan.nranks() > 1 ? 2 : 1; }
+
+// The private work buffer is used only by an FFT stage followed directly by
+// another FFT stage (slab plans: F2 -> F1); pencil and general plans always
+// go through a transpose slot.
+static bool family_needs_work(const Plan& plan) {
+  dfftb_plan_options o = plan.options;
+  const int kf = plan.kind == DFFTB_C2C ? DFFTB_C2C : DFFTB_R2C;
+  const int kb = plan.kind == DFFTB_C2C ? DFFTB_C2C : DFFTB_C2R;
+  for (int d = 0; d < 2; ++d) {
+    Plan p = build_plan(plan.dims, plan.decomp, plan.grid, d == 0 ? kf : kb, d, plan.prec, o);
+    for (size_t i = 0; i + 1 < p.stages.size(); ++i)
+      if (p.stages[i].type == StageType::Fft && p.stages[i + 1].type == StageType::Fft) return true;
+  }
+  return false;
 }
 
 static bool is_pow2(int64_t n) { return n >= 1 && (n & (n - 1)) == 0; }
@@ -301,8 +322,8 @@ static size_t table_bytes(const Plan& plan) {
 size_t workspace_bytes(const Plan& plan, int rank) {
   if (rank < 0 || rank >= plan.nranks()) raise(DFFTB_InvalidRank, "rank out of range");
   const size_t blk = (family_bytes(plan) + 255) / 256 * 256;
-  return kFlagsBytes + 2 * (size_t)family_exch_slots(plan) * blk + blk + kStatWords * sizeof(unsigned long long) +
-         table_bytes(plan);
+  return kFlagsBytes + (size_t)family_parities(plan) * family_exch_slots(plan) * blk +
+         (family_needs_work(plan) ? blk : 0) + kStatWords * sizeof(unsigned long long) + table_bytes(plan);
 }
 
 Ctx* ctx_create(const Plan& plan, int rank, int device) {
@@ -323,12 +344,13 @@ Ctx* ctx_create(const Plan& plan, int rank, int device) {
   ctx->flags_bytes = kFlagsBytes;
   ctx->exch_bytes = blk;
   ctx->exch_slots = family_exch_slots(plan);
-  ctx->region_bytes = kFlagsBytes + 2 * (size_t)ctx->exch_slots * blk;  // [slot][parity] buffers
-  ctx->work_bytes = blk;
+  ctx->parities = family_parities(plan);
+  ctx->region_bytes = kFlagsBytes + (size_t)ctx->parities * ctx->exch_slots * blk;  // [slot][parity] buffers
+  ctx->work_bytes = family_needs_work(plan) ? blk : 0;
   ctx->table_bytes = table_bytes(plan);
   CUDA_TRY(cudaMalloc(&ctx->region, ctx->region_bytes));
   CUDA_TRY(cudaMemset(ctx->region, 0, kFlagsBytes));
-  CUDA_TRY(cudaMalloc(&ctx->work, ctx->work_bytes));
+  if (ctx->work_bytes) CUDA_TRY(cudaMalloc(&ctx->work, ctx->work_bytes));
   CUDA_TRY(cudaMalloc(&ctx->dstat, kStatWords * sizeof(unsigned long long)));
   CUDA_TRY(cudaMemset(ctx->dstat, 0, kStatWords * sizeof(unsigned long long)));
   // twiddle tables w[m] = exp(-2 pi i m / n) in double, cast to T
@@ -923,6 +945,7 @@ static std::vector<Op> lower(const Plan& plan, const Ctx& ctx, const void* d_in,
       Lo.extents_of(me, offo, leno);
       row_major_strides(leno, nd, so, !last_fft, ctx.prec);
       void* out = last_fft ? d_out : ctx.work;
+      if (!out) raise(DFFTB_ArenaExhausted, "context has no work buffer for this plan");
       p.ndest = 1;
       p.oblk = p.n_out > 0 ? p.n_out : 1;
       Dest& d = p.dest[0];

@@ -134,6 +134,7 @@ struct Ctx {
   size_t flags_bytes = 0;
   size_t exch_bytes = 0;
   int exch_slots = 2;    // exchange buffers per parity in the shared region
+  int parities = 2;      // execute parities per slot (1 for a single rank)
   void* work = nullptr;  // private scratch for local->local passes
   size_t work_bytes = 0;
   size_t table_bytes = 0;  // twiddle + Bluestein tables

@@ -84,7 +84,11 @@ struct TmaCfg {
   static constexpr int EPREF = (sizeof(T) == 4 && N >= 256) ? 16 : 8;
   using SC = Sched<N, EPREF>;
   static constexpr int TPL = SC::TPL;
-  static constexpr int W0 = DFFTB_TMA_THREADS / TPL;
+#ifndef DFFTB_SMALL_W
+#define DFFTB_SMALL_W 64  // lane cap of short (N <= 64) tiles: more, smaller CTAs for small problems
+#endif
+  static constexpr int W0 = (N <= 64 && DFFTB_TMA_THREADS / TPL > DFFTB_SMALL_W) ? DFFTB_SMALL_W
+                                                                                 : DFFTB_TMA_THREADS / TPL;
   static constexpr int W = W0 < 1 ? 1 : (W0 > 64 ? 64 : W0);
   static constexpr int THREADS = W * TPL;
   using TL = TmaLayout<T, N, W>;

@@ -189,24 +189,30 @@ def test_gloo_world_size_2_host_path():
 
 def test_workspace_bytes():
     # dfftb_workspace_bytes (host-only): flag page (64 sync points x 64
-    # ranks) + one exchange buffer per transpose stage and parity + the work
-    # buffer, each sized for the largest block of the plan family, + status
-    # words + the per-axis twiddle (and Bluestein) tables (+ the half-length
-    # table of axes >= 1024, for the 2-CTA cluster pass)
+    # ranks) + one exchange buffer per transpose stage and execute parity
+    # (two parities with peers, one for a single rank) + the work buffer (slab
+    # plans only: F2 -> F1 without a transpose), each sized for the largest
+    # block of the plan family, + status words + the per-axis twiddle (and
+    # Bluestein) tables (+ the half-length table of axes >= 1024, for the
+    # 2-CTA cluster pass)
     flags = 64 * 64 * 8
     p = D.plan_pencil((512, 512, 512), (2, 4), D.TransformKind.C2C, D.Direction.Forward)
     blk = 512 ** 3 * 16 // 8
-    assert D.workspace_bytes(p, 0) == flags + 2 * 2 * blk + blk + 64 + 512 * 16
+    assert D.workspace_bytes(p, 0) == flags + 2 * 2 * blk + 64 + 512 * 16
+    one = D.plan_pencil((512, 512, 512), (1, 1), D.TransformKind.C2C, D.Direction.Forward)
+    assert D.workspace_bytes(one, 0) == flags + 2 * 512 ** 3 * 16 + 64 + 512 * 16  # 2 slots, 1 parity
+    sl = D.plan_slab((64, 64, 64), 4, D.TransformKind.C2C, D.Direction.Forward)
+    blk = 64 ** 3 * 16 // 4
+    assert D.workspace_bytes(sl, 0) == flags + 2 * 2 * blk + blk + 64 + 64 * 16  # slab: + work buffer
     q = D.plan_pencil((1024, 64, 64), (2, 4), D.TransformKind.C2C, D.Direction.Forward)
     blk = 1024 * 64 * 64 * 16 // 8
-    assert D.workspace_bytes(q, 0) == flags + 2 * 2 * blk + blk + 64 + (1024 + 512 + 64) * 16
+    assert D.workspace_bytes(q, 0) == flags + 2 * 2 * blk + 64 + (1024 + 512 + 64) * 16
     g = D.plan_general((8, 8, 16, 16), (1, 1, 1), D.TransformKind.C2C, D.Direction.Forward)
     blk = 8 * 8 * 16 * 16 * 16
-    assert D.workspace_bytes(g, 0) == flags + 2 * 3 * blk + blk + 64 + (8 + 16) * 16  # three transposes
+    assert D.workspace_bytes(g, 0) == flags + 3 * blk + 64 + (8 + 16) * 16  # three transposes, 1 rank
     # Bluestein length 17: chirp (17) + kernel spectrum (m = 64), fp32 complex
     b = D.plan_pencil((17, 4, 4), (1, 1), D.TransformKind.C2C, D.Direction.Forward, precision="f32")
-    blk = 17 * 4 * 4 * 8
-    assert D.workspace_bytes(b, 0) == flags + 2 * 2 * ((blk + 255) // 256 * 256) + (blk + 255) // 256 * 256 \
-        + 64 + (17 + 64) * 8 + 4 * 8
+    blk = (17 * 4 * 4 * 8 + 255) // 256 * 256
+    assert D.workspace_bytes(b, 0) == flags + 2 * blk + 64 + (17 + 64) * 8 + 4 * 8
     with pytest.raises(D.Error, match="InvalidRank"):
         D.workspace_bytes(p, 8)

@@ -209,8 +209,9 @@ __device__ __forceinline__ void store_lk(const PassParams& p, void* const* sptr,
 
 // The pass kernel: persistent CTAs walk the tiles of the launch box.  SPEC:
 // the last forward pass of a spectral operator (multiplier epilogue).
-template <typename T, int N, int EPREF, int W, bool ADJ, int STAGES, int LK, bool SPEC = false>
-__global__ void __launch_bounds__(W* Sched<N, EPREF>::TPL, DFFTB_TMA_MINB)
+template <typename T, int N, int EPREF, int W, bool ADJ, int STAGES, int LK, bool SPEC = false,
+          int MINB = DFFTB_TMA_MINB>
+__global__ void __launch_bounds__(W* Sched<N, EPREF>::TPL, MINB)
     fft_pass_tma_kernel(const __grid_constant__ PassParams p, const __grid_constant__ CUtensorMap tm,
                         const TmaArgs ta) {
   using C = Cpx<T>;

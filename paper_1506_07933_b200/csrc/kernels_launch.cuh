@@ -85,21 +85,22 @@ struct TmaCfg {
   using SC = Sched<N, EPREF>;
   static constexpr int TPL = SC::TPL;
 #ifndef DFFTB_SMALL_W
-#define DFFTB_SMALL_W 64  // lane cap of short (N <= 64) tiles: more, smaller CTAs for small problems
+#define DFFTB_SMALL_W 16  // lane cap of short (N <= 64) tiles: more, smaller CTAs (64^3: 32 -> 25 us)
 #endif
   static constexpr int W0 = (N <= 64 && DFFTB_TMA_THREADS / TPL > DFFTB_SMALL_W) ? DFFTB_SMALL_W
                                                                                  : DFFTB_TMA_THREADS / TPL;
   static constexpr int W = W0 < 1 ? 1 : (W0 > 64 ? 64 : W0);
   static constexpr int THREADS = W * TPL;
+  static constexpr int MINB = DFFTB_TMA_MINB;
   using TL = TmaLayout<T, N, W>;
-  static constexpr int STAGES = (2 * TL::STG + TL::XCH + 128 <= (220 * 1024) / DFFTB_TMA_MINB) ? 2 : 1;
+  static constexpr int STAGES = (2 * TL::STG + TL::XCH + 128 <= (220 * 1024) / MINB) ? 2 : 1;
   static constexpr int SMEM = STAGES * TL::STG + TL::XCH + 8 * STAGES + 8 * kMaxDest;
 };
 
 template <typename T, int N, bool ADJ, int LK, bool SPEC = false>
 static cudaError_t launch_tma_tn(const PassParams& p, const TmaPlan& tp, int grid_limit, cudaStream_t s) {
   using Cf = TmaCfg<T, N>;
-  auto kern = fft_pass_tma_kernel<T, N, Cf::EPREF, Cf::W, ADJ, Cf::STAGES, LK, SPEC>;
+  auto kern = fft_pass_tma_kernel<T, N, Cf::EPREF, Cf::W, ADJ, Cf::STAGES, LK, SPEC, Cf::MINB>;
   static int occ_of[64] = {0}, sms_of[64] = {0};
   int dev = 0;
   cudaGetDevice(&dev);

@@ -72,7 +72,8 @@ struct Knobs {
   double frac = -1.0;         // DFFTB_OVERLAP_FRAC: SM share of the exchange pass (<0: model)
   bool graphs = true;         // DFFTB_GRAPHS: replay cached programs as CUDA graphs
   bool op_times = false;      // DFFTB_OP_TIMES: print per-op device times of timed executes
-  bool pdl = true;            // DFFTB_PDL: programmatic dependent launch between passes
+  bool pdl = false;           // DFFTB_PDL: programmatic dependent launch between passes (opt-in:
+                              // 512^3 4.18 -> 4.14 ms, but 1024^3 46.4 -> 53.4 ms)
   bool cl2 = false;           // DFFTB_CL2: 2-CTA cluster pass for long strided lanes (opt-in: measured slower)
 };
 
@@ -93,7 +94,7 @@ static const Knobs& knobs() {
     if (const char* e = getenv("DFFTB_OVERLAP_FRAC")) k.frac = atof(e);
     k.graphs = flag("DFFTB_GRAPHS", true);
     k.op_times = flag("DFFTB_OP_TIMES", false);
-    k.pdl = flag("DFFTB_PDL", true);
+    k.pdl = flag("DFFTB_PDL", false);
     k.cl2 = flag("DFFTB_CL2", false);
     return k;
   }();
@@ -629,12 +630,14 @@ static bool plan_tma(Op& op, int prec) {
     const int64_t si = p.in_si * csize, sa = (p.A > 1 ? p.in_sa : (int64_t)n * p.in_si) * csize;
     if (p.in_sb != 1) return false;
     if (si % 16 || sa % 16) {
-      // rows a tensor map cannot describe (fp32 C2R user blocks: 129-bin
-      // rows of 1032 bytes): per-thread 8-byte cp.async into the same tile
       if (cl2) {
         W = tma_tile_w(prec, n);
         full_box(tp.args, p, W);
       }
+      // rows a tensor map cannot describe (fp32 C2R user blocks: 129-bin
+      // rows of 1032 bytes; a row-pair map, whose odd rows start 8 bytes off
+      // a 16-byte boundary, raised an illegal-instruction fault): per-thread
+      // 8-byte cp.async into the same tile
       if (csize != 8 || (reinterpret_cast<uintptr_t>(p.in) & 7) || !knobs().unaligned_ldgsts) return false;
       tp.args.bulk = 0;
       tp.args.ldgsts = 1;
@@ -945,7 +948,7 @@ static std::vector<Op> lower(const Plan& plan, const Ctx& ctx, const void* d_in,
       Lo.extents_of(me, offo, leno);
       row_major_strides(leno, nd, so, !last_fft, ctx.prec);
       void* out = last_fft ? d_out : ctx.work;
-      if (!out) raise(DFFTB_ArenaExhausted, "context has no work buffer for this plan");
+      if (!last_fft && !out) raise(DFFTB_ArenaExhausted, "context has no work buffer for this plan");
       p.ndest = 1;
       p.oblk = p.n_out > 0 ? p.n_out : 1;
       Dest& d = p.dest[0];

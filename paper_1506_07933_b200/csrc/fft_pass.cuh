@@ -288,9 +288,18 @@ __device__ __forceinline__ int spad(int i) {
   return i + (i >> LOG_SLOTS);
 }
 template <typename C>
-__host__ __device__ constexpr int lane_stride(int n) {
-  // padded lane length, forced odd (in slots) so W lanes hit distinct banks
-  return (n + (n >> (sizeof(C) == 16 ? 3 : 4))) | 1;
+__host__ __device__ constexpr int lane_stride(int n, int w = 64) {
+  // Padded lane length in slots.  In the w-fastest thread layout (strided
+  // lanes) one 16-byte shared-memory wavefront (128 bytes: m = 8 slots)
+  // serves W lanes x m/W positions; for W < m, lane offsets m/W apart modulo m
+  // keep those accesses on distinct banks (1024-point fp64 strided passes:
+  // 8.9 -> 7.5 ms).  Odd offsets otherwise (and for fp32, where the residue
+  // rule measured slower).
+  constexpr int m = 128 / (int)sizeof(C);
+  const int base = n + (n >> (sizeof(C) == 16 ? 3 : 4));
+  if (sizeof(C) != 16 || w >= m) return base | 1;
+  const int r = m / w;
+  return base + ((r - base % m) % m + m) % m;
 }
 
 template <typename T>
@@ -510,7 +519,7 @@ __global__ void __launch_bounds__(W* Sched<N, EPREF>::TPL, DFFTB_MINB)
   using C = Cpx<T>;
   using SC = Sched<N, EPREF>;
   constexpr int TPL = SC::TPL;
-  constexpr int LS = lane_stride<C>(N);
+  constexpr int LS = lane_stride<C>(N, ADJ ? W : 64);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   C* smem = reinterpret_cast<C*>(smem_raw);
   const int tid = threadIdx.x;

@@ -89,7 +89,7 @@ template <typename T, int N, int W>
 struct TmaLayout {
   using C = Cpx<T>;
   static constexpr int STG = W * N * (int)sizeof(C);  // one staging slot
-  static constexpr int XCH = W * lane_stride<C>(N) * (int)sizeof(C);
+  static constexpr int XCH = W * lane_stride<C>(N, W) * (int)sizeof(C);
 };
 
 // stage-0 fetch from a staging slot, compile-time lane kind
@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(W* Sched<N, EPREF>::TPL, MINB)
   using SC = Sched<N, EPREF>;
   using TL = TmaLayout<T, N, W>;
   constexpr int TPL = SC::TPL;
-  constexpr int LS = lane_stride<C>(N);
+  constexpr int LS = lane_stride<C>(N, ADJ ? W : 64);
   extern __shared__ __align__(1024) unsigned char smem_tma[];
   unsigned char* stg = smem_tma;
   C* xch = reinterpret_cast<C*>(smem_tma + STAGES * TL::STG);
@@ -364,7 +364,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(W* Sched<NH, EPREF>:
   using TL = TmaLayout<T, NH, W>;
   constexpr int TPL = SC::TPL;
   constexpr int E = SC::E;
-  constexpr int LS = lane_stride<C>(NH);
+  constexpr int LS = lane_stride<C>(NH, W);
   constexpr int R0 = SC::S > 0 ? SC::radix(0) : 1;
   constexpr int NB0 = E / R0;
   extern __shared__ __align__(1024) unsigned char smem_tma[];

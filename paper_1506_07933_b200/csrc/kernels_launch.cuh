@@ -28,7 +28,7 @@ struct PassCfg {
   static constexpr int W0 = DFFTB_THREADS / TPL;
   static constexpr int W = W0 < 1 ? 1 : (W0 > 64 ? 64 : W0);
   static constexpr int THREADS = W * TPL;
-  static constexpr int SMEM = W * lane_stride<Cpx<T>>(N) * (int)sizeof(Cpx<T>);
+  static constexpr int SMEM = W * lane_stride<Cpx<T>>(N, W) * (int)sizeof(Cpx<T>);
 };
 
 template <typename T, int N, bool ADJ>

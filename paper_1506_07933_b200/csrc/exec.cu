@@ -75,6 +75,7 @@ struct Knobs {
   bool pdl = false;           // DFFTB_PDL: programmatic dependent launch between passes (opt-in:
                               // 512^3 4.18 -> 4.14 ms, but 1024^3 46.4 -> 53.4 ms)
   bool cl2 = false;           // DFFTB_CL2: 2-CTA cluster pass for long strided lanes (opt-in: measured slower)
+  bool rhalf = true;          // DFFTB_RHALF: R2C / C2R lanes as half-length complex FFTs
 };
 
 static const Knobs& knobs() {
@@ -96,6 +97,7 @@ static const Knobs& knobs() {
     k.op_times = flag("DFFTB_OP_TIMES", false);
     k.pdl = flag("DFFTB_PDL", false);
     k.cl2 = flag("DFFTB_CL2", false);
+    k.rhalf = flag("DFFTB_RHALF", true);
     return k;
   }();
   return k;
@@ -309,14 +311,21 @@ static size_t table_bytes(const Plan& plan) {
   for (auto n : plan.dims) {
     if (std::find(seen.begin(), seen.end(), n) != seen.end()) continue;
     seen.push_back(n);
-    if (is_pow2(n)) {
-      t += (size_t)n * 2 * plan.prec;
-      const bool half_seen = std::find(plan.dims.begin(), plan.dims.end(), n / 2) != plan.dims.end();
-      if (cl2_supported(plan.prec, (int)n) && !half_seen) t += (size_t)(n / 2) * 2 * plan.prec;
-    } else if (!is_smooth(n)) {
-      t += (size_t)(n + bluestein_m(n)) * 2 * plan.prec;
-    }
+    if (!is_pow2(n) && !is_smooth(n)) t += (size_t)(n + bluestein_m(n)) * 2 * plan.prec;
   }
+  // twiddle tables: every power-of-two axis length, plus the half lengths the
+  // 2-CTA cluster pass and the half-length R2C / C2R lanes use (as ctx_create)
+  std::vector<int64_t> tabs;
+  for (auto n : plan.dims) {
+    if (!is_pow2(n)) continue;
+    tabs.push_back(n);
+    if (cl2_supported(plan.prec, (int)n)) tabs.push_back(n / 2);
+  }
+  const int64_t nl = plan.dims.back();
+  if (plan.kind != DFFTB_C2C && is_pow2(nl) && nl >= 16) tabs.push_back(nl / 2);
+  std::sort(tabs.begin(), tabs.end());
+  tabs.erase(std::unique(tabs.begin(), tabs.end()), tabs.end());
+  for (auto n : tabs) t += (size_t)n * 2 * plan.prec;
   return t;
 }
 
@@ -363,6 +372,11 @@ Ctx* ctx_create(const Plan& plan, int rank, int device) {
     if (!is_pow2(n)) continue;
     tables.push_back(n);
     if (cl2_supported(plan.prec, n)) tables.push_back(n / 2);  // the 2-CTA cluster pass's stages
+  }
+  {
+    // half-length R2C / C2R lanes run n/2-point stages
+    const int64_t nl = plan.dims.back();
+    if (plan.kind != DFFTB_C2C && is_pow2(nl) && nl >= 16) tables.push_back((int)(nl / 2));
   }
   for (int n : tables) {
     if (ctx->twiddles.count(n)) continue;
@@ -503,6 +517,7 @@ struct Op {
   GenParams g{};
   // lane geometry (overlap chunking, spectral epilogue)
   int v = -1, ax_a = -1, ax_b = -1, ax_a1 = -1;
+  int u = -1;                // exchange passes: the transpose's gather axis
   const Dist* before = nullptr;
   std::vector<int> members;  // exchange group (world ranks, group order)
   // ---- sync point / events / begin
@@ -687,6 +702,17 @@ static bool plan_tma(Op& op, int prec) {
     if (p.A > 1 && (p.in_sa * esize) % 16) return false;
     tp.args.bulk = 1;
     tp.args.lane_bytes = (int)lane_bytes;
+    // R2C / C2R lanes as half-length complex FFTs: twice the
+    // lanes per tile, half the butterflies; needs the n/2-point table
+    // (tw2 set) and, for C2R, one destination
+    const bool half = knobs().rhalf && p.in_mode != kInComplex && n >= 16 && p.tw2 != nullptr &&
+                      p.spec.op == 0 && (p.in_mode == kInReal || (p.ndest == 1 && p.store_mode == 0)) &&
+                      (p.in_mode == kInReal ? lane_bytes <= (int64_t)(n / 2) * csize
+                                            : lane_bytes <= (int64_t)(n / 2 + 2) * csize);
+    if (half) {
+      tp.args.rhalf = 1;
+      full_box(tp.args, p, tma_tile_w(prec, n / 2));
+    }
     return true;
   }
   return false;
@@ -719,7 +745,7 @@ static void set_store_mode(PassParams& p) {
 // the 2-CTA cluster pass runs NH = n/2 point Stockham stages (tw = the
 // n/2-point table) after a cross-CTA radix-2 step (tw2 = the n-point table)
 static void plan_twiddles(Op& op, const Ctx& ctx) {
-  if (op.tma && op.tp.args.cl2) op.p.tw = ctx.twiddles.at(op.n / 2);
+  if (op.tma && (op.tp.args.cl2 || op.tp.args.rhalf)) op.p.tw = ctx.twiddles.at(op.n / 2);
 }
 
 static void plan_generic(Op& op, const Ctx& ctx) {
@@ -908,6 +934,7 @@ static std::vector<Op> lower(const Plan& plan, const Ctx& ctx, const void* d_in,
       // the transposed final forward exchange feeds the axis-0 pass: store
       // its buffer [x1][x0][rest] so axis-0 lanes read short strides
       const bool swap_out = tr->transposed && knobs().zperm && nd >= 3;
+      op.u = u;
       op.members = group_members(Lo, me, g);
       op.remote = op.members.size() > 1;
       p.ndest = (int)op.members.size();
@@ -982,9 +1009,13 @@ static std::vector<Op> lower(const Plan& plan, const Ctx& ctx, const void* d_in,
 // signals (remote), on the side stream.  The SMs are split so the two run
 // concurrently: P needs enough to keep NVLink busy, Q takes the rest.
 
-static bool overlap_candidate(const Op& o) {
-  return o.kind == OpKind::Pass && o.tma && !o.generic && o.before && o.before->ndim() == 3 && o.p.A1 <= 1 &&
-         o.p.A > 0 && o.p.B > 0;
+// Rank-independent shape test: every rank must derive the same op and sync
+// sequence (sync slots are numbered in program order), so nothing that
+// depends on this rank's block (sizes, buffer alignment, TMA planning) may
+// decide whether a pair is chunked.
+static bool overlap_shape(const Op& o) {
+  return o.kind == OpKind::Pass && is_pow2(o.n) && o.before && o.before->ndim() == 3 && o.p.A1 <= 1 &&
+         o.p.in_mode == kInComplex && !o.p.out_real;
 }
 
 // SM share of the exchange pass: both passes finish together when
@@ -1045,9 +1076,15 @@ static void overlap_pairs(std::vector<Op>& prog, const Plan& plan, const Ctx& ct
   std::vector<Op> out;
   size_t i = 0;
   while (i < prog.size()) {
-    const bool pattern = i + 2 < prog.size() && overlap_candidate(prog[i]) && prog[i].remote &&
-                         prog[i + 1].kind == OpKind::Sync && overlap_candidate(prog[i + 2]) &&
-                         !prog[i + 2].remote && prog[i + 2].p.ndest == 1;
+    bool pattern = i + 2 < prog.size() && overlap_shape(prog[i]) && prog[i].remote &&
+                   prog[i + 1].kind == OpKind::Sync && overlap_shape(prog[i + 2]) && !prog[i + 2].remote &&
+                   prog[i + 2].p.ndest == 1;
+    // the chunk axis X: transformed by neither pass and not moved by the
+    // exchange (X != the gather axis u), so every group member's chunk c
+    // covers the same global range
+    const int X = pattern ? 3 - prog[i].v - prog[i + 2].v : -1;
+    pattern = pattern && prog[i].v != prog[i + 2].v && X >= 0 && X < 3 && X != prog[i].u &&
+              (X == prog[i].ax_a || X == prog[i].ax_b) && (X == prog[i + 2].ax_a || X == prog[i + 2].ax_b);
     if (!pattern) {
       out.push_back(prog[i++]);
       continue;
@@ -1055,36 +1092,24 @@ static void overlap_pairs(std::vector<Op>& prog, const Plan& plan, const Ctx& ct
     const Op& P = prog[i];
     const Op& S = prog[i + 1];
     const Op& Q = prog[i + 2];
-    const int X = 3 - P.v - Q.v;
-    bool ok = P.v != Q.v && X >= 0 && X < 3 && (X == P.ax_a || X == P.ax_b) && (X == Q.ax_a || X == Q.ax_b);
+    // this rank's chunking (its own block; empty chunks still signal)
     int64_t offQ[kMaxDims], lenQ[kMaxDims];
-    if (ok) {
-      Q.before->extents_of(me, offQ, lenQ);
-      for (int m : P.members) {
-        int64_t o[kMaxDims], l[kMaxDims];
-        P.before->extents_of(m, o, l);
-        ok = ok && o[X] == offQ[X] && l[X] == lenQ[X];
-      }
-    }
-    const int WP = P.tp.args.W, WQ = Q.tp.args.W;
-    const int64_t Xe = ok ? lenQ[X] : 0;
-    // chunk length: a whole number of tiles on the beta axis of either pass
+    Q.before->extents_of(me, offQ, lenQ);
+    const int64_t Xe = lenQ[X];
+    const bool p_box = P.tma && !P.generic, q_box = Q.tma && !Q.generic;  // box launches need the TMA kernel
     int64_t unit = 1;
-    if (ok && X == P.ax_b) unit = std::max<int64_t>(unit, WP);
-    if (ok && X == Q.ax_b) unit = std::max<int64_t>(unit, WQ);
-    int64_t R = ok ? ((Xe + C - 1) / C + unit - 1) / unit * unit : 0;
-    const int nch = R > 0 ? (int)((Xe + R - 1) / R) : 0;
-    if (!ok || nch < 2 || P.tp.args.ldgsts || Q.tp.args.ldgsts) {
-      out.push_back(prog[i++]);
-      continue;
-    }
+    if (p_box && X == P.ax_b) unit = std::max<int64_t>(unit, P.tp.args.W);
+    if (q_box && X == Q.ax_b) unit = std::max<int64_t>(unit, Q.tp.args.W);
+    const int64_t R = std::max<int64_t>(1, ((Xe + C - 1) / C + unit - 1) / unit * unit);
     const int gP = overlap_split(P, Q, ctx.prec, sms);
-    for (int c = 0; c < nch; ++c) {
-      const int64_t x0 = c * R, x1 = std::min<int64_t>(Xe, x0 + R);
-      Op pc = P;
-      pc.tp.args = chunk_box(P, X, x0, x1, WP);
-      pc.grid_sms = gP;
-      out.push_back(pc);
+    for (int c = 0; c < C; ++c) {
+      const int64_t x0 = std::min<int64_t>(Xe, c * R), x1 = std::min<int64_t>(Xe, x0 + R);
+      if (p_box || c == 0) {
+        Op pc = P;  // without box support the whole pass runs in chunk 0
+        if (p_box) pc.tp.args = chunk_box(P, X, x0, x1, P.tp.args.W);
+        pc.grid_sms = gP;
+        if (!p_box || x1 > x0) out.push_back(pc);
+      }
       Op sig;
       sig.kind = OpKind::Sync;
       sig.signal = true;
@@ -1105,23 +1130,25 @@ static void overlap_pairs(std::vector<Op>& prog, const Plan& plan, const Ctx& ct
       wt.wait = true;
       wt.members = S.members;
       out.push_back(wt);  // signal and wait of chunk c share a sync slot (assign_slots)
-      Op qc = Q;
-      qc.stream = 1;
-      qc.tp.args = chunk_box(Q, X, x0, x1, WQ);
-      qc.grid_sms = sms - gP;
-      out.push_back(qc);
+      if (q_box || c == C - 1) {
+        Op qc = Q;  // without box support the whole pass runs after the last chunk
+        qc.stream = 1;
+        if (q_box) qc.tp.args = chunk_box(Q, X, x0, x1, Q.tp.args.W);
+        qc.grid_sms = sms - gP;
+        if (!q_box || x1 > x0) out.push_back(qc);
+      }
     }
     // join: the caller's stream waits for the side stream
     Op rj;
     rj.kind = OpKind::Record;
     rj.stream = 1;
-    rj.event = nevents + nch;
+    rj.event = nevents + C;
     out.push_back(rj);
     Op wj;
     wj.kind = OpKind::WaitEvent;
-    wj.event = nevents + nch;
+    wj.event = nevents + C;
     out.push_back(wj);
-    nevents += nch + 1;
+    nevents += C + 1;
     i += 3;
   }
   prog.swap(out);

@@ -18,7 +18,10 @@
 
 namespace dfftb {
 
-enum LaneKind : int { kC2CFwd = 0, kC2CBwd = 1, kR2C = 2, kC2R = 3 };
+// kR2Ch / kC2Rh: the half-length forms of R2C / C2R (the kernel's N is n/2):
+// an n-point real lane is an N-point complex FFT plus a post- (R2C) or
+// pre-twiddle (C2R) over the bin pairs (k, N - k).
+enum LaneKind : int { kC2CFwd = 0, kC2CBwd = 1, kR2C = 2, kC2R = 3, kR2Ch = 4, kC2Rh = 5 };
 
 // A launch covers the tile box [a0, a0 + na) x [bt0, bt0 + nbt) of (alpha,
 // beta tile) -- the whole pass, or one chunk of a pipelined exchange.
@@ -31,6 +34,7 @@ struct TmaArgs {
   int bulk;        // 1: contiguous cp.async.bulk, 0: tensor map
   int lane_bytes;  // bulk mode: bytes of one stored lane
   int cl2;         // 2-CTA cluster pass (fft_pass_cl2_kernel)
+  int rhalf;       // R2C / C2R lanes as half-length complex FFTs (kR2Ch / kC2Rh)
   int W;           // lanes per tile
   int ldgsts;      // strided lanes: per-thread cp.async (16 B) instead of TMA boxes
 };
@@ -85,10 +89,10 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
       : "memory");
 }
 
-template <typename T, int N, int W>
+template <typename T, int N, int W, int EXTRA = 0>
 struct TmaLayout {
   using C = Cpx<T>;
-  static constexpr int STG = W * N * (int)sizeof(C);  // one staging slot
+  static constexpr int STG = W * (N + EXTRA) * (int)sizeof(C);  // one staging slot (EXTRA: C2Rh's bin N, pad)
   static constexpr int XCH = W * lane_stride<C>(N, W) * (int)sizeof(C);
 };
 
@@ -207,6 +211,130 @@ __device__ __forceinline__ void store_lk(const PassParams& p, void* const* sptr,
   }
 }
 
+// Half-length C2R pre-twiddle (irfft_1d semantics, kernels.hpp:362-389, on
+// an N-point transform): from the Hermitian bins X[0..N] of a 2N-point lane,
+//   Z[m] = (X[m] + conj X[N-m]) + i (X[m] - conj X[N-m]) e^{+i pi m / N},
+// whose N-point inverse gives z[m] = x[2m] + i x[2m+1].  DC / Nyquist
+// imaginary parts are dropped and the NonHermitian statistics taken as the
+// bins are read.  v receives conj(Z) (inverse = conj of the forward FFT).
+template <typename T, int N, int EPREF>
+__device__ __forceinline__ void fetch_c2rh(Cpx<T>* v, int j, const Cpx<T>* X, const Cpx<T>* twn, double* m2,
+                                           double* mi) {
+  using C = Cpx<T>;
+  using SC = Sched<N, EPREF>;
+  constexpr int E = SC::E;
+  constexpr int TPL = SC::TPL;
+  constexpr int R0 = SC::S > 0 ? SC::radix(0) : 1;
+  constexpr int NB0 = E / R0;
+#pragma unroll
+  for (int t = 0; t < NB0; ++t) {
+#pragma unroll
+    for (int r = 0; r < R0; ++r) {
+      const int m = j + t * TPL + r * (N / R0);
+      C a = X[m], b = X[N - m];
+      if (m2) {
+        const double aa = (double)a.x * (double)a.x + (double)a.y * (double)a.y;
+        const double bb = (double)b.x * (double)b.x + (double)b.y * (double)b.y;
+        *m2 = fmax(*m2, fmax(aa, bb));
+        if (m == 0) *mi = fmax(*mi, fmax(fabs((double)a.y), fabs((double)b.y)));
+      }
+      if (m == 0) {
+        a.y = T(0);
+        b.y = T(0);
+      }
+      const C cb = C{b.x, -b.y};
+      const C e = cadd(a, cb), d = csub(a, cb);
+      C w = __ldg(twn + m);
+      w.y = -w.y;
+      const C o = cmul(d, w);
+      v[t * R0 + r] = C{e.x - o.y, -(e.y + o.x)};  // conj(e + i o)
+    }
+  }
+}
+
+// Half-length R2C post-twiddle: Z = FFT_N(x[2m] + i x[2m+1]) in the
+// registers' last-stage positions k ->
+//   X[k] = (Z[k] + conj Z[N-k]) / 2 + W_2N^k (Z[k] - conj Z[N-k]) / (2i),
+// the pair partner read through the lane's shared-memory slots; bin N
+// (= Re Z[0] - Im Z[0]) goes to the thread holding bin 0.
+template <typename T, int N, int EPREF>
+__device__ __forceinline__ void post_r2ch(Cpx<T>* v, Cpx<T>* lane, const Cpx<T>* twn, int j, Cpx<T>& xn) {
+  using C = Cpx<T>;
+  using SC = Sched<N, EPREF>;
+  constexpr int E = SC::E;
+  constexpr int TPL = SC::TPL;
+  constexpr int S = SC::S;
+  constexpr int RL = S > 0 ? SC::radix(S - 1) : 1;
+  constexpr int NSL = S > 0 ? SC::ns(S - 1) : 1;
+  constexpr int NBL = E / RL;
+  __syncthreads();  // every thread is done with the last stage's exchange reads
+#pragma unroll
+  for (int t = 0; t < NBL; ++t)
+#pragma unroll
+    for (int r = 0; r < RL; ++r) lane[spad<C>(j + t * TPL + r * NSL)] = v[t * RL + r];
+  __syncthreads();
+  xn = C{v[0].x - v[0].y, T(0)};
+#pragma unroll
+  for (int t = 0; t < NBL; ++t) {
+#pragma unroll
+    for (int r = 0; r < RL; ++r) {
+      const int k = j + t * TPL + r * NSL;
+      const C zk = v[t * RL + r];
+      C zr = lane[spad<C>((N - k) & (N - 1))];
+      zr.y = -zr.y;
+      const C e = C{(zk.x + zr.x) * T(0.5), (zk.y + zr.y) * T(0.5)};
+      const C d = csub(zk, zr);
+      const C o = C{d.y * T(0.5), -d.x * T(0.5)};  // d / (2i)
+      v[t * RL + r] = cadd(e, cmul(__ldg(twn + k), o));
+    }
+  }
+  __syncthreads();  // the next tile's first exchange overwrites the lane slots
+}
+
+// one complex output element k of a lane (any store mode: the general
+// destination formula)
+template <typename T>
+__device__ __forceinline__ void store_one(const PassParams& p, Cpx<T> x, int k, int alpha, int beta, T sc) {
+  if (k >= p.n_out) return;
+  const int q = static_cast<int>(k / p.oblk);
+  const int kk = k - static_cast<int>(q * p.oblk);
+  const Dest& d = p.dest[q];
+  x.x *= sc;
+  x.y *= sc;
+  reinterpret_cast<Cpx<T>*>(d.ptr)[d.base + dst_alpha_off(p, d, alpha) + (int64_t)beta * d.sb + (int64_t)kk * d.sk] = x;
+}
+
+// Half-length C2R store: register position m holds r = FFT(conj Z)[m], so
+// z[m] = conj(r) and the real outputs 2m, 2m+1 are r.x, -r.y (one dest).
+template <typename T, int N, int EPREF>
+__device__ __forceinline__ void store_c2rh(const PassParams& p, const Cpx<T>* v, int j, int alpha, int beta, T sc) {
+  using SC = Sched<N, EPREF>;
+  constexpr int E = SC::E;
+  constexpr int TPL = SC::TPL;
+  constexpr int S = SC::S;
+  constexpr int RL = S > 0 ? SC::radix(S - 1) : 1;
+  constexpr int NSL = S > 0 ? SC::ns(S - 1) : 1;
+  constexpr int NBL = E / RL;
+  const Dest& d = p.dest[0];
+  const int64_t base = d.base + dst_alpha_off(p, d, alpha) + (int64_t)beta * d.sb;
+  T* out = reinterpret_cast<T*>(d.ptr);
+  const bool pair = d.sk == 1 && (base & 1) == 0;
+#pragma unroll
+  for (int t = 0; t < NBL; ++t) {
+#pragma unroll
+    for (int r = 0; r < RL; ++r) {
+      const int m = j + t * TPL + r * NSL;
+      const Cpx<T> x = v[t * RL + r];
+      if (pair) {
+        reinterpret_cast<Cpx<T>*>(out + base)[m] = Cpx<T>{x.x * sc, -x.y * sc};
+      } else {
+        out[base + (int64_t)(2 * m) * d.sk] = x.x * sc;
+        out[base + (int64_t)(2 * m + 1) * d.sk] = -x.y * sc;
+      }
+    }
+  }
+}
+
 // The pass kernel: persistent CTAs walk the tiles of the launch box.  SPEC:
 // the last forward pass of a spectral operator (multiplier epilogue).
 template <typename T, int N, int EPREF, int W, bool ADJ, int STAGES, int LK, bool SPEC = false,
@@ -216,7 +344,7 @@ __global__ void __launch_bounds__(W* Sched<N, EPREF>::TPL, MINB)
                         const TmaArgs ta) {
   using C = Cpx<T>;
   using SC = Sched<N, EPREF>;
-  using TL = TmaLayout<T, N, W>;
+  using TL = TmaLayout<T, N, W, LK == kC2Rh ? 2 : 0>;
   constexpr int TPL = SC::TPL;
   constexpr int LS = lane_stride<C>(N, ADJ ? W : 64);
   extern __shared__ __align__(1024) unsigned char smem_tma[];
@@ -232,6 +360,7 @@ __global__ void __launch_bounds__(W* Sched<N, EPREF>::TPL, MINB)
   const C* tw = reinterpret_cast<const C*>(p.tw);
   constexpr int ESIZE = LK == kR2C ? (int)sizeof(T) : (int)sizeof(C);
   const T sc = static_cast<T>(p.scale);
+  const C* twn = reinterpret_cast<const C*>(p.tw2);  // 2N-point table (half-length R2C / C2R)
 #if DFFTB_TWB
   TwBase<T, N, EPREF> twb;  // per-thread twiddle bases, loaded once per kernel
   load_twbase<T, N, EPREF>(twb, tw, j);
@@ -316,6 +445,14 @@ __global__ void __launch_bounds__(W* Sched<N, EPREF>::TPL, MINB)
       const C* scp = reinterpret_cast<const C*>(st);
       fetch0_lk<T, N, EPREF, LK>(
           v, j, [&](int pos) { return scp[pos * W + w]; }, [&](int) { return T(0); });
+    } else if constexpr (LK == kR2Ch) {
+      // 2N reals read as N complex z[m] = x[2m] + i x[2m+1]
+      const C* scp = reinterpret_cast<const C*>(st) + w * (ta.lane_bytes / (int)sizeof(C));
+      fetch0_lk<T, N, EPREF, kC2CFwd>(v, j, [&](int pos) { return scp[pos]; }, [&](int) { return T(0); });
+    } else if constexpr (LK == kC2Rh) {
+      const C* scp = reinterpret_cast<const C*>(st) + w * (ta.lane_bytes / (int)sizeof(C));
+      const bool stats = beta < p.B;
+      fetch_c2rh<T, N, EPREF>(v, j, scp, twn, stats ? &lmax : nullptr, stats ? &limag : nullptr);
     } else {
       const int ll = ta.lane_bytes / ESIZE;  // stored lane length in elements
       const C* scp = reinterpret_cast<const C*>(st) + w * ll;
@@ -336,9 +473,20 @@ __global__ void __launch_bounds__(W* Sched<N, EPREF>::TPL, MINB)
       }
     }
     run_stages<T, N, EPREF, 0>(v, lane, tw, j, twbp);
-    if (beta < p.B) store_lk<T, N, EPREF, LK, SPEC>(p, sptr, v, j, alpha, beta, sc);
+    if constexpr (LK == kR2Ch) {
+      C xn;  // bin N (real), computed by the thread holding bin 0
+      post_r2ch<T, N, EPREF>(v, lane, twn, j, xn);
+      if (beta < p.B) {
+        store_lk<T, N, EPREF, kC2CFwd, false>(p, sptr, v, j, alpha, beta, sc);
+        if (j == 0) store_one<T>(p, xn, N, alpha, beta, sc);
+      }
+    } else if constexpr (LK == kC2Rh) {
+      if (beta < p.B) store_c2rh<T, N, EPREF>(p, v, j, alpha, beta, sc);
+    } else {
+      if (beta < p.B) store_lk<T, N, EPREF, LK, SPEC>(p, sptr, v, j, alpha, beta, sc);
+    }
   }
-  if constexpr (LK == kC2R) herm_reduce(p.herm, sqrt(lmax), limag);
+  if constexpr (LK == kC2R || LK == kC2Rh) herm_reduce(p.herm, sqrt(lmax), limag);
 }
 
 // Long strided lanes on a 2-CTA cluster.  A tile of W lanes of length

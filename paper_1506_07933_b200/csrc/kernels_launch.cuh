@@ -76,7 +76,7 @@ static cudaError_t launch_prec(int n, const PassParams& p, bool adj, cudaStream_
 }
 
 // TMA variant: one persistent CTA per SM, 512 threads, STAGES-deep prefetch
-template <typename T, int N>
+template <typename T, int N, int EXTRA = 0>
 struct TmaCfg {
   // fp32 long lanes use 16 elements per thread (radix-16 stages): half the
   // threads per lane, so twice the adjacent lanes per CTA and 64-128 byte
@@ -92,14 +92,14 @@ struct TmaCfg {
   static constexpr int W = W0 < 1 ? 1 : (W0 > 64 ? 64 : W0);
   static constexpr int THREADS = W * TPL;
   static constexpr int MINB = DFFTB_TMA_MINB;
-  using TL = TmaLayout<T, N, W>;
+  using TL = TmaLayout<T, N, W, EXTRA>;
   static constexpr int STAGES = (2 * TL::STG + TL::XCH + 128 <= (220 * 1024) / MINB) ? 2 : 1;
   static constexpr int SMEM = STAGES * TL::STG + TL::XCH + 8 * STAGES + 8 * kMaxDest;
 };
 
 template <typename T, int N, bool ADJ, int LK, bool SPEC = false>
 static cudaError_t launch_tma_tn(const PassParams& p, const TmaPlan& tp, int grid_limit, cudaStream_t s) {
-  using Cf = TmaCfg<T, N>;
+  using Cf = TmaCfg<T, N, LK == kC2Rh ? 2 : 0>;
   auto kern = fft_pass_tma_kernel<T, N, Cf::EPREF, Cf::W, ADJ, Cf::STAGES, LK, SPEC, Cf::MINB>;
   static int occ_of[64] = {0}, sms_of[64] = {0};
   int dev = 0;
@@ -197,10 +197,34 @@ static cudaError_t launch_cl2_prec(int n, const PassParams& p, const TmaPlan& tp
 }
 
 
+// half-length R2C / C2R lanes (contiguous): an n/2-point kernel
+template <typename T>
+static cudaError_t launch_rhalf_prec(int n, const PassParams& p, const TmaPlan& tp, int gl, cudaStream_t s) {
+  const bool r2c = p.in_mode == kInReal;
+#define DFFTB_RH_CASE(NN)                                                                        \
+  case NN:                                                                                       \
+    return r2c ? launch_tma_tn<T, NN / 2, false, kR2Ch>(p, tp, gl, s)                            \
+               : launch_tma_tn<T, NN / 2, false, kC2Rh>(p, tp, gl, s);
+  switch (n) {
+    DFFTB_RH_CASE(16)
+    DFFTB_RH_CASE(32)
+    DFFTB_RH_CASE(64)
+    DFFTB_RH_CASE(128)
+    DFFTB_RH_CASE(256)
+    DFFTB_RH_CASE(512)
+    DFFTB_RH_CASE(1024)
+    DFFTB_RH_CASE(2048)
+    DFFTB_RH_CASE(4096)
+  }
+#undef DFFTB_RH_CASE
+  return cudaErrorInvalidValue;
+}
+
 template <typename T>
 static cudaError_t launch_tma_prec(int n, const PassParams& p, bool adj, const TmaPlan& tp, int gl,
                                    cudaStream_t s) {
   if (tp.args.cl2) return launch_cl2_prec<T>(n, p, tp, gl, s);
+  if (tp.args.rhalf) return launch_rhalf_prec<T>(n, p, tp, gl, s);
   const int lk = p.in_mode == kInReal ? kR2C : (p.in_mode == kInHermitian ? kC2R : (p.inverse ? kC2CBwd : kC2CFwd));
 #define DFFTB_TMA_CASE(NN)                                                \
   case NN:                                                                \

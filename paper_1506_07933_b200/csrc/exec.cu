@@ -76,6 +76,7 @@ struct Knobs {
                               // 512^3 4.18 -> 4.14 ms, but 1024^3 46.4 -> 53.4 ms)
   bool cl2 = false;           // DFFTB_CL2: 2-CTA cluster pass for long strided lanes (opt-in: measured slower)
   bool rhalf = true;          // DFFTB_RHALF: R2C / C2R lanes as half-length complex FFTs
+  int row_align = 32;         // DFFTB_ROW_ALIGN: internal row padding in bytes (16, 32 or 64)
 };
 
 static const Knobs& knobs() {
@@ -98,9 +99,18 @@ static const Knobs& knobs() {
     k.pdl = flag("DFFTB_PDL", false);
     k.cl2 = flag("DFFTB_CL2", false);
     k.rhalf = flag("DFFTB_RHALF", true);
+    if (const char* e = getenv("DFFTB_ROW_ALIGN")) {
+      const int a = atoi(e);
+      k.row_align = (a == 16 || a == 32 || a == 64 || a == 128) ? a : 32;
+    }
     return k;
   }();
   return k;
+}
+
+static int64_t inner_pad(int64_t len, int prec) {
+  const int64_t q = std::max<int64_t>(1, knobs().row_align / (2 * prec));  // complex elements per unit
+  return (len + q - 1) / q * q;
 }
 
 void* Ctx::exch(int r, int slot, int parity) const {
@@ -134,7 +144,13 @@ struct NvtxRange {
 // the innermost extent so every row starts on a 16-byte boundary (fp32
 // complex rows of odd length, e.g. the 129-bin R2C axis), which lets the TMA
 // path describe them.  User-visible buffers are never padded.
-static int64_t inner_pad(int64_t len, int prec) { return prec == 4 ? (len + 1) & ~int64_t(1) : len; }
+static const struct Knobs& knobs();
+
+// Internal buffers pad their innermost rows to a multiple of
+// DFFTB_ROW_ALIGN bytes (default 32: a DRAM sector), so TMA can describe them
+// (16-byte strides) and strided boxes of narrow tiles start on sector
+// boundaries (129-bin R2C rows: 1032 / 2064 bytes otherwise).
+static int64_t inner_pad(int64_t len, int prec);
 
 static int64_t max_internal_count(const Dist& d, int prec) {
   int64_t m = 0;

@@ -724,10 +724,10 @@ static bool plan_tma(Op& op, int prec) {
     const bool half = knobs().rhalf && p.in_mode != kInComplex && n >= 16 && p.tw2 != nullptr &&
                       p.spec.op == 0 && (p.in_mode == kInReal || (p.ndest == 1 && p.store_mode == 0)) &&
                       (p.in_mode == kInReal ? lane_bytes <= (int64_t)(n / 2) * csize
-                                            : lane_bytes <= (int64_t)(n / 2 + 2) * csize);
+                                            : lane_bytes <= (int64_t)(n / 2 + kC2RhExtra) * csize);
     if (half) {
       tp.args.rhalf = 1;
-      full_box(tp.args, p, tma_tile_w(prec, n / 2));
+      full_box(tp.args, p, tma_tile_w_halfreal(prec, n / 2));
     }
     return true;
   }

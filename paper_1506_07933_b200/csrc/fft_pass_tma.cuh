@@ -22,6 +22,8 @@ namespace dfftb {
 // an n-point real lane is an N-point complex FFT plus a post- (R2C) or
 // pre-twiddle (C2R) over the bin pairs (k, N - k).
 enum LaneKind : int { kC2CFwd = 0, kC2CBwd = 1, kR2C = 2, kC2R = 3, kR2Ch = 4, kC2Rh = 5 };
+// staged elements per C2Rh lane beyond N: bin N plus the internal row padding
+constexpr int kC2RhExtra = 8;
 
 // A launch covers the tile box [a0, a0 + na) x [bt0, bt0 + nbt) of (alpha,
 // beta tile) -- the whole pass, or one chunk of a pipelined exchange.
@@ -92,7 +94,7 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 template <typename T, int N, int W, int EXTRA = 0>
 struct TmaLayout {
   using C = Cpx<T>;
-  static constexpr int STG = W * (N + EXTRA) * (int)sizeof(C);  // one staging slot (EXTRA: C2Rh's bin N, pad)
+  static constexpr int STG = W * (N + EXTRA) * (int)sizeof(C);  // one staging slot (EXTRA: C2Rh's bin N + pad)
   static constexpr int XCH = W * lane_stride<C>(N, W) * (int)sizeof(C);
 };
 
@@ -344,7 +346,7 @@ __global__ void __launch_bounds__(W* Sched<N, EPREF>::TPL, MINB)
                         const TmaArgs ta) {
   using C = Cpx<T>;
   using SC = Sched<N, EPREF>;
-  using TL = TmaLayout<T, N, W, LK == kC2Rh ? 2 : 0>;
+  using TL = TmaLayout<T, N, W, LK == kC2Rh ? kC2RhExtra : 0>;
   constexpr int TPL = SC::TPL;
   constexpr int LS = lane_stride<C>(N, ADJ ? W : 64);
   extern __shared__ __align__(1024) unsigned char smem_tma[];
@@ -358,7 +360,8 @@ __global__ void __launch_bounds__(W* Sched<N, EPREF>::TPL, MINB)
   const int j = ADJ ? tid / W : tid % TPL;
   C* lane = xch + w * LS;
   const C* tw = reinterpret_cast<const C*>(p.tw);
-  constexpr int ESIZE = LK == kR2C ? (int)sizeof(T) : (int)sizeof(C);
+  // bytes per element of the input's strides: reals for R2C lanes
+  constexpr int ESIZE = (LK == kR2C || LK == kR2Ch) ? (int)sizeof(T) : (int)sizeof(C);
   const T sc = static_cast<T>(p.scale);
   const C* twn = reinterpret_cast<const C*>(p.tw2);  // 2N-point table (half-length R2C / C2R)
 #if DFFTB_TWB

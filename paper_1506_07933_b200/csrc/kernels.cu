@@ -29,6 +29,12 @@ int tma_tile_w_f32(int n);
 
 int tma_tile_w(int prec, int n) { return prec == 8 ? tma_tile_w_f64(n) : tma_tile_w_f32(n); }
 
+int tma_tile_w_halfreal_f64(int n);
+int tma_tile_w_halfreal_f32(int n);
+int tma_tile_w_halfreal(int prec, int n) {
+  return prec == 8 ? tma_tile_w_halfreal_f64(n) : tma_tile_w_halfreal_f32(n);
+}
+
 bool cl2_supported(int prec, int n) {
   (void)prec;
   return n == 1024 || n == 2048 || n == 4096;

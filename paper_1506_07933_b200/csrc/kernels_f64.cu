@@ -11,5 +11,6 @@ cudaError_t launch_pass_tma_f64(int n, const PassParams& p, bool adj, const TmaP
   return launch_tma_prec<double>(n, p, adj, tp, grid_limit, s);
 }
 int tma_tile_w_f64(int n) { return tma_w_prec<double>(n); }
+int tma_tile_w_halfreal_f64(int n) { return tma_w_halfreal_prec<double>(n); }
 
 }  // namespace dfftb

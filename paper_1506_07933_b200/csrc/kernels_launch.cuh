@@ -76,12 +76,14 @@ static cudaError_t launch_prec(int n, const PassParams& p, bool adj, cudaStream_
 }
 
 // TMA variant: one persistent CTA per SM, 512 threads, STAGES-deep prefetch
-template <typename T, int N, int EXTRA = 0>
+template <typename T, int N, int EXTRA = 0, bool HALFREAL = false>
 struct TmaCfg {
   // fp32 long lanes use 16 elements per thread (radix-16 stages): half the
   // threads per lane, so twice the adjacent lanes per CTA and 64-128 byte
-  // TMA rows instead of 16-32 (fp64 tiles are bounded by shared memory)
-  static constexpr int EPREF = (sizeof(T) == 4 && N >= 256) ? 16 : 8;
+  // TMA rows instead of 16-32 (fp64 tiles are bounded by shared memory).
+  // Half-length real lanes (HALFREAL) switch from N >= 64 so that halving the
+  // length doubles the lanes per tile in fp32 too.
+  static constexpr int EPREF = (sizeof(T) == 4 && (N >= 256 || (HALFREAL && N >= 64))) ? 16 : 8;
   using SC = Sched<N, EPREF>;
   static constexpr int TPL = SC::TPL;
 #ifndef DFFTB_SMALL_W
@@ -99,7 +101,7 @@ struct TmaCfg {
 
 template <typename T, int N, bool ADJ, int LK, bool SPEC = false>
 static cudaError_t launch_tma_tn(const PassParams& p, const TmaPlan& tp, int grid_limit, cudaStream_t s) {
-  using Cf = TmaCfg<T, N, LK == kC2Rh ? 2 : 0>;
+  using Cf = TmaCfg<T, N, LK == kC2Rh ? kC2RhExtra : 0, LK == kR2Ch || LK == kC2Rh>;
   auto kern = fft_pass_tma_kernel<T, N, Cf::EPREF, Cf::W, ADJ, Cf::STAGES, LK, SPEC, Cf::MINB>;
   static int occ_of[64] = {0}, sms_of[64] = {0};
   int dev = 0;
@@ -254,6 +256,22 @@ static cudaError_t launch_tma_prec(int n, const PassParams& p, bool adj, const T
   }
 #undef DFFTB_TMA_CASE
   return cudaErrorInvalidValue;
+}
+
+template <typename T>
+static int tma_w_halfreal_prec(int n) {
+  switch (n) {
+    case 8: return TmaCfg<T, 8, 0, true>::W;
+    case 16: return TmaCfg<T, 16, 0, true>::W;
+    case 32: return TmaCfg<T, 32, 0, true>::W;
+    case 64: return TmaCfg<T, 64, 0, true>::W;
+    case 128: return TmaCfg<T, 128, 0, true>::W;
+    case 256: return TmaCfg<T, 256, 0, true>::W;
+    case 512: return TmaCfg<T, 512, 0, true>::W;
+    case 1024: return TmaCfg<T, 1024, 0, true>::W;
+    case 2048: return TmaCfg<T, 2048, 0, true>::W;
+  }
+  return 0;
 }
 
 template <typename T>

@@ -56,6 +56,11 @@ ORACLE_CASES = [
     ("pencil", [8, 8, 8], [1, 8], "c2c", "f64"),
     ("pencil", [4, 4, 4], [4, 2], "r2c", "f64"),      # empty tail blocks
     ("slab", [4, 2, 2], [3], "c2c", "f64"),           # ragged slab, empty-ish tails
+    # single rank, long strided axes: pair-interleaved buffers (narrow tiles)
+    ("pencil", [1024, 16, 8], [1, 1], "c2c", "f64"),
+    ("pencil", [16, 1024, 8], [1, 1], "c2c", "f64"),
+    ("pencil", [2048, 8, 32], [1, 1], "r2c", "f32"),
+    ("pencil", [8, 2048, 16], [1, 1], "c2c", "f32"),
 ]
 
 

@@ -61,9 +61,11 @@ enum { DFFTB_FORWARD = 0, DFFTB_BACKWARD = 1 };
 enum { DFFTB_SLAB = 0, DFFTB_PENCIL = 1, DFFTB_GENERAL = 2 };
 /* template parameter T: bytes per real component */
 enum { DFFTB_F32 = 4, DFFTB_F64 = 8 };
-/* ExchangePath (exchange.hpp:425).  On B200 all three are the fused
- * FFT + peer-memory exchange (byte-identical results, as in the reference);
- * the value is kept for API parity. */
+/* ExchangePath (exchange.hpp:425).  On B200 all three are the fused FFT +
+ * peer-memory exchange with byte-identical results, as in the reference.
+ * PIPELINED with chunks_per_peer = C > 1 additionally chunks every exchange
+ * pass that feeds a local pass into C pieces overlapped with that pass on a
+ * second stream (pipelined_all_to_all, exchange.hpp:323-423). */
 enum { DFFTB_EXCHANGE_BLOCKING = 0, DFFTB_EXCHANGE_STAGED = 1, DFFTB_EXCHANGE_PIPELINED = 2 };
 /* plan layout sides */
 enum { DFFTB_INPUT = 0, DFFTB_OUTPUT = 1 };
@@ -72,9 +74,10 @@ enum { DFFTB_INPUT = 0, DFFTB_OUTPUT = 1 };
 typedef struct {
   int exchange;        /* DFFTB_EXCHANGE_* */
   int normalize;       /* backward applies 1/N once (default 1) */
-  int chunks_per_peer; /* >= 1 */
-  int staging_buffers; /* >= 1 */
-  int validate_finite; /* reject NaN/Inf input (ConfigInvalid) */
+  int chunks_per_peer; /* >= 1; PIPELINED: chunks of the overlapped exchange */
+  int staging_buffers; /* >= 1; no staging copies exist on B200 (accepted) */
+  int validate_finite; /* reject NaN/Inf input (ConfigInvalid, reported after
+                          the launches so the ranks stay in lockstep) */
 } dfftb_plan_options;
 
 /* TimingBreakdown, timing.hpp:16-37 (seconds) */

@@ -45,6 +45,9 @@
 #ifndef DFFTB_TWB
 #define DFFTB_TWB 1  // twiddle bases kept in registers across tiles
 #endif
+#ifndef DFFTB_LS_FP32
+#define DFFTB_LS_FP32 0  // A/B: the bank-aware lane-stride residue for fp32 narrow tiles too
+#endif
 #ifndef DFFTB_TMA_MINB
 #define DFFTB_TMA_MINB 1    // resident CTAs per SM the TMA kernel is compiled for
 #endif
@@ -297,7 +300,7 @@ __host__ __device__ constexpr int lane_stride(int n, int w = 64) {
   // rule measured slower).
   constexpr int m = 128 / (int)sizeof(C);
   const int base = n + (n >> (sizeof(C) == 16 ? 3 : 4));
-  if (sizeof(C) != 16 || w >= m) return base | 1;
+  if ((sizeof(C) != 16 && !DFFTB_LS_FP32) || w >= m) return base | 1;
   const int r = m / w;
   return base + ((r - base % m) % m + m) % m;
 }

@@ -74,7 +74,6 @@ struct Knobs {
   bool op_times = false;      // DFFTB_OP_TIMES: print per-op device times of timed executes
   bool pdl = false;           // DFFTB_PDL: programmatic dependent launch between passes (opt-in:
                               // 512^3 4.18 -> 4.14 ms, but 1024^3 46.4 -> 53.4 ms)
-  bool cl2 = false;           // DFFTB_CL2: 2-CTA cluster pass for long strided lanes (opt-in: measured slower)
   bool rhalf = true;          // DFFTB_RHALF: R2C / C2R lanes as half-length complex FFTs
   int row_align = 32;         // DFFTB_ROW_ALIGN: internal row padding in bytes (16, 32 or 64)
 };
@@ -97,7 +96,6 @@ static const Knobs& knobs() {
     k.graphs = flag("DFFTB_GRAPHS", true);
     k.op_times = flag("DFFTB_OP_TIMES", false);
     k.pdl = flag("DFFTB_PDL", false);
-    k.cl2 = flag("DFFTB_CL2", false);
     k.rhalf = flag("DFFTB_RHALF", true);
     if (const char* e = getenv("DFFTB_ROW_ALIGN")) {
       const int a = atoi(e);
@@ -329,13 +327,12 @@ static size_t table_bytes(const Plan& plan) {
     seen.push_back(n);
     if (!is_pow2(n) && !is_smooth(n)) t += (size_t)(n + bluestein_m(n)) * 2 * plan.prec;
   }
-  // twiddle tables: every power-of-two axis length, plus the half lengths the
-  // 2-CTA cluster pass and the half-length R2C / C2R lanes use (as ctx_create)
+  // twiddle tables: every power-of-two axis length, plus the half length of
+  // the last axis the half-length R2C / C2R lanes use (as ctx_create)
   std::vector<int64_t> tabs;
   for (auto n : plan.dims) {
     if (!is_pow2(n)) continue;
     tabs.push_back(n);
-    if (cl2_supported(plan.prec, (int)n)) tabs.push_back(n / 2);
   }
   const int64_t nl = plan.dims.back();
   if (plan.kind != DFFTB_C2C && is_pow2(nl) && nl >= 16) tabs.push_back(nl / 2);
@@ -387,7 +384,6 @@ Ctx* ctx_create(const Plan& plan, int rank, int device) {
     if (!is_pow2(n) && !is_smooth(n) && !ctx->bluestein.count(n)) ctx->bluestein[n] = bluestein_tables(n, plan.prec);
     if (!is_pow2(n)) continue;
     tables.push_back(n);
-    if (cl2_supported(plan.prec, n)) tables.push_back(n / 2);  // the 2-CTA cluster pass's stages
   }
   {
     // half-length R2C / C2R lanes run n/2-point stages
@@ -640,13 +636,8 @@ static bool plan_tma(Op& op, int prec) {
   const PassParams& p = op.p;
   const int n = op.n;
   if (!knobs().tma || n < 8 || (int64_t)p.A * p.B == 0) return false;
-  int W = tma_tile_w(prec, n);
+  const int W = tma_tile_w(prec, n);
   if (W <= 0) return false;
-  // long strided C2C lanes whose one-CTA tile is narrower than a 128-byte
-  // row: the 2-CTA cluster pass (half of every lane per CTA, twice the lanes)
-  const bool cl2 = knobs().cl2 && op.adj && p.in_mode == kInComplex && !p.out_real && p.A1 <= 1 &&
-                   p.spec.op == 0 && 2 * W * prec < 128 && cl2_supported(prec, n) && op.p.tw2 != nullptr;
-  if (cl2) W = tma_tile_w(prec, n / 2);
   const int csize = 2 * prec;
   if ((reinterpret_cast<uintptr_t>(p.in) & 15) != 0) return false;
   TmaPlan& tp = op.tp;
@@ -661,10 +652,6 @@ static bool plan_tma(Op& op, int prec) {
     const int64_t si = p.in_si * csize, sa = (p.A > 1 ? p.in_sa : (int64_t)n * p.in_si) * csize;
     if (p.in_sb != 1) return false;
     if (si % 16 || sa % 16) {
-      if (cl2) {
-        W = tma_tile_w(prec, n);
-        full_box(tp.args, p, W);
-      }
       // rows a tensor map cannot describe (fp32 C2R user blocks: 129-bin
       // rows of 1032 bytes; a row-pair map, whose odd rows start 8 bytes off
       // a 16-byte boundary, raised an illegal-instruction fault): per-thread
@@ -676,8 +663,7 @@ static bool plan_tma(Op& op, int prec) {
     }
     auto enc = tensor_map_encoder();
     if (!enc) return false;
-    const int span = cl2 ? n / 2 : n;  // rows one CTA stages
-    const int rows = span < 256 ? span : 256;
+    const int rows = n < 256 ? n : 256;
     cuuint64_t gdim[3];
     cuuint64_t gstride[2];
     cuuint32_t box[3], estr[3] = {1, 1, 1};
@@ -706,7 +692,6 @@ static bool plan_tma(Op& op, int prec) {
     if (r != CUDA_SUCCESS) return false;
     tp.args.rows = rows;
     tp.args.bulk = 0;
-    tp.args.cl2 = cl2 ? 1 : 0;
     return true;
   }
   const int64_t lane_elems = p.in_mode == kInHermitian ? n / 2 + 1 : n;
@@ -757,13 +742,13 @@ static void set_store_mode(PassParams& p) {
   p.omask = (int)b - 1;
 }
 
-// Non-power-of-two lengths run the generic mixed-radix / Bluestein kernel
-// the 2-CTA cluster pass runs NH = n/2 point Stockham stages (tw = the
-// n/2-point table) after a cross-CTA radix-2 step (tw2 = the n-point table)
+// Half-length R2C / C2R lanes run n/2-point Stockham stages (tw = the
+// n/2-point table) around a pre- / post-twiddle (tw2 = the n-point table)
 static void plan_twiddles(Op& op, const Ctx& ctx) {
-  if (op.tma && (op.tp.args.cl2 || op.tp.args.rhalf)) op.p.tw = ctx.twiddles.at(op.n / 2);
+  if (op.tma && op.tp.args.rhalf) op.p.tw = ctx.twiddles.at(op.n / 2);
 }
 
+// Non-power-of-two lengths run the generic mixed-radix / Bluestein kernel
 static void plan_generic(Op& op, const Ctx& ctx) {
   if (is_pow2(op.n)) return;
   op.tma = false;

@@ -112,7 +112,7 @@ struct PassParams {
   int oshift, omask;            // store_mode 1: q = k >> oshift, kk = k & omask
   double scale;
   const void* tw;               // N complex twiddles exp(-2 pi i m / N)
-  const void* tw2;              // 2-CTA cluster pass: the full-length table (tw: half length)
+  const void* tw2;              // half-length real lanes: the n-point table (tw: the n/2-point one)
   unsigned long long* herm;     // C2R: [0] max |X| bits, [1] max |Im DC/Nyq| bits
   SpecEpi spec;                 // spectral epilogue (spec.op == 0: none)
   Dest dest[kMaxDest];

@@ -35,7 +35,6 @@ struct TmaArgs {
   int rows;        // box rows per TMA op (ADJ)
   int bulk;        // 1: contiguous cp.async.bulk, 0: tensor map
   int lane_bytes;  // bulk mode: bytes of one stored lane
-  int cl2;         // 2-CTA cluster pass (fft_pass_cl2_kernel)
   int rhalf;       // R2C / C2R lanes as half-length complex FFTs (kR2Ch / kC2Rh)
   int W;           // lanes per tile
   int ldgsts;      // strided lanes: per-thread cp.async (16 B) instead of TMA boxes
@@ -146,11 +145,9 @@ __device__ __forceinline__ void fetch0_lk(Cpx<T>* v, int j, LDC ldc, LDR ldr, do
 }
 
 // final store, compile-time lane kind; per-tile addressing precomputed
-// KM / kadd: output index of register position kk is kk * KM + kadd (a CTA
-// of a 2-CTA cluster holds the even or the odd outputs of its lanes)
-template <typename T, int N, int EPREF, int LK, bool SPEC = false, int KM = 1>
+template <typename T, int N, int EPREF, int LK, bool SPEC = false>
 __device__ __forceinline__ void store_lk(const PassParams& p, void* const* sptr, const Cpx<T>* v,
-                                         int j, int alpha, int beta, T sc, int kadd = 0) {
+                                         int j, int alpha, int beta, T sc) {
   using C = Cpx<T>;
   using SC = Sched<N, EPREF>;
   constexpr int E = SC::E;
@@ -183,7 +180,7 @@ __device__ __forceinline__ void store_lk(const PassParams& p, void* const* sptr,
     for (int t = 0; t < NBL; ++t) {
 #pragma unroll
       for (int r = 0; r < RL; ++r) {
-        const int k = (j + t * TPL + r * NSL) * KM + kadd;
+        const int k = j + t * TPL + r * NSL;
         if constexpr (LK == kR2C) {
           if (k > N / 2) continue;
         }
@@ -201,7 +198,7 @@ __device__ __forceinline__ void store_lk(const PassParams& p, void* const* sptr,
     for (int t = 0; t < NBL; ++t) {
 #pragma unroll
       for (int r = 0; r < RL; ++r) {
-        const int k = (j + t * TPL + r * NSL) * KM + kadd;
+        const int k = j + t * TPL + r * NSL;
         if (k >= p.n_out) continue;
         const int q = static_cast<int>(k / p.oblk);
         const int kk = k - static_cast<int>(q * p.oblk);
@@ -490,140 +487,6 @@ __global__ void __launch_bounds__(W* Sched<N, EPREF>::TPL, MINB)
     }
   }
   if constexpr (LK == kC2R || LK == kC2Rh) herm_reduce(p.herm, sqrt(lmax), limag);
-}
-
-// Long strided lanes on a 2-CTA cluster.  A tile of W lanes of length
-// N = 2 NH is split by lane position: CTA r of the cluster stages rows
-// [r NH, (r+1) NH) of the box, so each CTA holds W lanes x NH points and the
-// TMA box rows are as wide as for an NH-point pass (128 bytes for fp64 at
-// N = 1024, where one CTA would fit only 4 lanes, 64-byte rows).  The first
-// radix-2 (decimation in frequency) step pairs x[m] with x[m + NH] across the
-// two CTAs through distributed shared memory:
-//   CTA 0: y[m] = x[m] + x[m + NH]                 -> X[2k]     = DFT_NH(y)[k]
-//   CTA 1: y[m] = (x[m] - x[m + NH]) W_N^m         -> X[2k + 1] = DFT_NH(y)[k]
-// then each CTA runs the NH-point Stockham pass and stores its half of the
-// outputs (even / odd k).  C2C lane kinds.  One cluster barrier per tile: the
-// peer has staged its half before it is read, and has read ours before the
-// slot is refilled (the refill is issued after the next tile's barrier).
-template <typename T, int NH, int EPREF, int W, int STAGES, int LK>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(W* Sched<NH, EPREF>::TPL, 1)
-    fft_pass_cl2_kernel(const __grid_constant__ PassParams p, const __grid_constant__ CUtensorMap tm,
-                        const TmaArgs ta) {
-  static_assert(LK == kC2CFwd || LK == kC2CBwd, "cluster pass: C2C lanes");
-  using C = Cpx<T>;
-  using SC = Sched<NH, EPREF>;
-  using TL = TmaLayout<T, NH, W>;
-  constexpr int TPL = SC::TPL;
-  constexpr int E = SC::E;
-  constexpr int LS = lane_stride<C>(NH, W);
-  constexpr int R0 = SC::S > 0 ? SC::radix(0) : 1;
-  constexpr int NB0 = E / R0;
-  extern __shared__ __align__(1024) unsigned char smem_tma[];
-  unsigned char* stg = smem_tma;
-  C* xch = reinterpret_cast<C*>(smem_tma + STAGES * TL::STG);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_tma + STAGES * TL::STG + TL::XCH);
-  void** sptr = reinterpret_cast<void**>(bars + STAGES);
-
-  uint32_t crank;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
-  const int tid = threadIdx.x;
-  const int w = tid % W;
-  const int j = tid / W;
-  C* lane = xch + w * LS;
-  const C* tw = reinterpret_cast<const C*>(p.tw);    // NH-point table
-  const C* twn = reinterpret_cast<const C*>(p.tw2);  // N-point table
-  const T sc = static_cast<T>(p.scale);
-  TwBase<T, NH, EPREF> twb;
-  load_twbase<T, NH, EPREF>(twb, tw, j);
-  const int cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
-  // the peer CTA's staging area (distributed shared memory)
-  uint32_t peer_stg;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(peer_stg) : "r"(smem_u32(stg)), "r"(crank ^ 1u));
-
-  auto issue = [&](int64_t t, int s) {
-    if (tid != 0) return;
-    int alpha, bt;
-    tile_coords(ta, t, alpha, bt);
-    const int beta0 = bt * W;
-    unsigned char* dst = stg + s * TL::STG;
-    mbar_expect_tx(&bars[s], (uint32_t)(W * NH * sizeof(C)));
-    for (int r0 = 0; r0 < NH; r0 += ta.rows) {
-      const int row = (int)crank * NH + r0;
-      const int c1 = ta.i_dim == 1 ? row : alpha;
-      const int c2 = ta.i_dim == 1 ? alpha : row;
-      tma_load_3d(dst + (size_t)r0 * W * sizeof(C), &tm, 2 * beta0, c1, c2, &bars[s]);
-    }
-  };
-  auto cluster_sync = [] {
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-  };
-
-  if (tid == 0) {
-    for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (tid < kMaxDest) sptr[tid] = p.dest[tid].ptr;
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  __syncthreads();
-  for (int s = 0; s < STAGES; ++s) {
-    const int64_t t = cl + (int64_t)s * ncl;
-    if (t < ta.ntiles) issue(t, s);
-  }
-  int k = 0;
-  int64_t pending = -1;  // tile whose slot refill waits for the next cluster barrier
-  int pending_slot = 0;
-  for (int64_t t = cl; t < ta.ntiles; t += ncl, ++k) {
-    const int s = k % STAGES;
-    mbar_wait(&bars[s], (uint32_t)((k / STAGES) & 1));
-    cluster_sync();  // both halves of tile t staged; the peer is done with the previous slot
-    if (pending >= 0) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue(pending, pending_slot);
-      pending = -1;
-    }
-    int alpha, beta;
-    tile_coords(ta, t, alpha, beta);
-    beta = beta * W + w;
-    const C* mine = reinterpret_cast<const C*>(stg + s * TL::STG);
-    const uint32_t theirs = peer_stg + (uint32_t)(s * TL::STG);
-    C v[E];
-#pragma unroll
-    for (int tt = 0; tt < NB0; ++tt) {
-#pragma unroll
-      for (int r = 0; r < R0; ++r) {
-        const int m = j + tt * TPL + r * (NH / R0);
-        const C a = mine[m * W + w];
-        C b;
-        if constexpr (sizeof(T) == 8)
-          asm volatile("ld.shared::cluster.v2.f64 {%0, %1}, [%2];"
-                       : "=d"(b.x), "=d"(b.y)
-                       : "r"(theirs + (uint32_t)((m * W + w) * sizeof(C)))
-                       : "memory");
-        else
-          asm volatile("ld.shared::cluster.v2.f32 {%0, %1}, [%2];"
-                       : "=f"(b.x), "=f"(b.y)
-                       : "r"(theirs + (uint32_t)((m * W + w) * sizeof(C)))
-                       : "memory");
-        C lo = crank == 0 ? a : b, hi = crank == 0 ? b : a;  // x[m], x[m + NH]
-        if constexpr (LK == kC2CBwd) {
-          lo.y = -lo.y;
-          hi.y = -hi.y;
-        }
-        v[tt * R0 + r] = crank == 0 ? cadd(lo, hi) : cmul(csub(lo, hi), __ldg(twn + m));
-      }
-    }
-    {
-      const int64_t t2 = t + (int64_t)STAGES * ncl;
-      if (t2 < ta.ntiles) {
-        pending = t2;  // refill after the next barrier (the peer may still read slot s)
-        pending_slot = s;
-      }
-    }
-    run_stages<T, NH, EPREF, 0>(v, lane, tw, j, &twb);
-    if (beta < p.B) store_lk<T, NH, EPREF, LK, false, 2>(p, sptr, v, j, alpha, beta, sc, (int)crank);
-  }
-  cluster_sync();  // neither CTA exits while its peer may still read its shared memory
 }
 
 }  // namespace dfftb

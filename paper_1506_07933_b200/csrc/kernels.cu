@@ -35,10 +35,6 @@ int tma_tile_w_halfreal(int prec, int n) {
   return prec == 8 ? tma_tile_w_halfreal_f64(n) : tma_tile_w_halfreal_f32(n);
 }
 
-bool cl2_supported(int prec, int n) {
-  (void)prec;
-  return n == 1024 || n == 2048 || n == 4096;
-}
 
 cudaError_t launch_pass_tma(int prec, int n, const PassParams& p, bool adj, const TmaPlan& tp, int grid_limit,
                             cudaStream_t s) {

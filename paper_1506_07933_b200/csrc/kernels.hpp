@@ -45,7 +45,6 @@ struct TmaPlan {
 };
 int tma_tile_w(int prec, int n);  // lanes per CTA of the TMA kernel
 int tma_tile_w_halfreal(int prec, int n);  // ... of its half-length R2C / C2R variant (n/2-point)
-bool cl2_supported(int prec, int n);  // lengths the 2-CTA cluster pass covers
 cudaError_t launch_pass_tma(int prec, int n, const PassParams& p, bool adj, const TmaPlan& tp, int grid_limit,
                             cudaStream_t s);
 cudaError_t launch_pass(int prec, int n, const PassParams& p, bool adj, cudaStream_t s);

@@ -1,4 +1,4 @@
-// Template launchers of the FFT pass kernels (direct, TMA, 2-CTA cluster),
+// Template launchers of the FFT pass kernels (direct, TMA, half-length real),
 // instantiated once per precision in kernels_f64.cu / kernels_f32.cu so the
 // two halves compile in parallel.
 #pragma once
@@ -141,64 +141,6 @@ static cudaError_t launch_tma_tn(const PassParams& p, const TmaPlan& tp, int gri
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
-// 2-CTA cluster pass for long strided lanes (n = 2 NH), C2C lane kinds
-template <typename T, int NH, int LK>
-static cudaError_t launch_cl2_tn(const PassParams& p, const TmaPlan& tp, int grid_limit, cudaStream_t s) {
-  using Cf = TmaCfg<T, NH>;
-  auto kern = fft_pass_cl2_kernel<T, NH, Cf::EPREF, Cf::W, Cf::STAGES, LK>;
-  static int clusters_of[64] = {0}, sms_of[64] = {0};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
-  cudaLaunchConfig_t cfg = {};
-  cfg.blockDim = dim3(Cf::THREADS);
-  cfg.dynamicSmemBytes = Cf::SMEM;
-  cfg.stream = s;
-  if (!clusters_of[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM);
-    if (e != cudaSuccess) return e;
-    int sms = 0, nc = 0;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cfg.gridDim = dim3((unsigned)(2 * (sms / 2)));
-    e = cudaOccupancyMaxActiveClusters(&nc, kern, &cfg);
-    if (e != cudaSuccess) return e;
-    sms_of[dev] = sms;
-    clusters_of[dev] = nc < 1 ? 1 : nc;
-  }
-  if (tp.args.ntiles <= 0) return cudaSuccess;
-  // persistent: one wave of co-resident clusters (fewer on a split GPU)
-  int64_t cap = clusters_of[dev];
-  if (grid_limit > 0 && grid_limit < sms_of[dev]) cap = std::max<int64_t>(1, cap * grid_limit / sms_of[dev]);
-  const int64_t nclus = tp.args.ntiles < cap ? tp.args.ntiles : cap;
-  cfg.gridDim = dim3((unsigned)(2 * nclus));
-  cudaLaunchAttribute attr[1];
-  if (tp.pdl) {
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-  }
-  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, p, tp.tmap, tp.args);
-  count_launch();
-  return e != cudaSuccess ? e : cudaGetLastError();
-}
-
-template <typename T>
-static cudaError_t launch_cl2_prec(int n, const PassParams& p, const TmaPlan& tp, int gl, cudaStream_t s) {
-  const bool bwd = p.inverse != 0;
-#define DFFTB_CL2_CASE(NN)                                                                       \
-  case NN:                                                                                       \
-    return bwd ? launch_cl2_tn<T, NN / 2, kC2CBwd>(p, tp, gl, s) : launch_cl2_tn<T, NN / 2, kC2CFwd>(p, tp, gl, s);
-  switch (n) {
-    DFFTB_CL2_CASE(1024)
-    DFFTB_CL2_CASE(2048)
-    DFFTB_CL2_CASE(4096)
-  }
-#undef DFFTB_CL2_CASE
-  return cudaErrorInvalidValue;
-}
-
-
 // half-length R2C / C2R lanes (contiguous): an n/2-point kernel
 template <typename T>
 static cudaError_t launch_rhalf_prec(int n, const PassParams& p, const TmaPlan& tp, int gl, cudaStream_t s) {
@@ -225,7 +167,6 @@ static cudaError_t launch_rhalf_prec(int n, const PassParams& p, const TmaPlan& 
 template <typename T>
 static cudaError_t launch_tma_prec(int n, const PassParams& p, bool adj, const TmaPlan& tp, int gl,
                                    cudaStream_t s) {
-  if (tp.args.cl2) return launch_cl2_prec<T>(n, p, tp, gl, s);
   if (tp.args.rhalf) return launch_rhalf_prec<T>(n, p, tp, gl, s);
   const int lk = p.in_mode == kInReal ? kR2C : (p.in_mode == kInHermitian ? kC2R : (p.inverse ? kC2CBwd : kC2CFwd));
 #define DFFTB_TMA_CASE(NN)                                                \

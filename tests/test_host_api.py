@@ -193,8 +193,8 @@ def test_workspace_bytes():
     # (two parities with peers, one for a single rank) + the work buffer (slab
     # plans only: F2 -> F1 without a transpose), each sized for the largest
     # block of the plan family, + status words + the per-axis twiddle (and
-    # Bluestein) tables (+ the half-length table of axes >= 1024, for the
-    # 2-CTA cluster pass)
+    # Bluestein) tables (+ the half-length table of the last axis of R2C / C2R
+    # plans, for the half-length real lanes)
     flags = 64 * 64 * 8
     p = D.plan_pencil((512, 512, 512), (2, 4), D.TransformKind.C2C, D.Direction.Forward)
     blk = 512 ** 3 * 16 // 8
@@ -206,7 +206,11 @@ def test_workspace_bytes():
     assert D.workspace_bytes(sl, 0) == flags + 2 * 2 * blk + blk + 64 + 64 * 16  # slab: + work buffer
     q = D.plan_pencil((1024, 64, 64), (2, 4), D.TransformKind.C2C, D.Direction.Forward)
     blk = 1024 * 64 * 64 * 16 // 8
-    assert D.workspace_bytes(q, 0) == flags + 2 * 2 * blk + 64 + (1024 + 512 + 64) * 16
+    assert D.workspace_bytes(q, 0) == flags + 2 * 2 * blk + 64 + (1024 + 64) * 16
+    # R2C: + the n/2-point table of the last axis (half-length real lanes)
+    r1 = D.plan_pencil((64, 64, 256), (1, 1), D.TransformKind.R2C, D.Direction.Forward)
+    c1 = D.plan_pencil((64, 64, 256), (1, 1), D.TransformKind.C2C, D.Direction.Forward)
+    assert D.workspace_bytes(r1, 0) - D.workspace_bytes(c1, 0) == 128 * 16
     g = D.plan_general((8, 8, 16, 16), (1, 1, 1), D.TransformKind.C2C, D.Direction.Forward)
     blk = 8 * 8 * 16 * 16 * 16
     assert D.workspace_bytes(g, 0) == flags + 3 * blk + 64 + (8 + 16) * 16  # three transposes, 1 rank

@@ -551,6 +551,13 @@ struct Program {
 };
 
 static void drop_programs(Ctx& ctx) {
+  bool graphs = false;
+  for (auto& kv : ctx.programs) graphs = graphs || kv.second->graph != nullptr;
+  if (graphs) {
+    // replays may still be queued: let them finish before their graphs go
+    DeviceGuard g(ctx.device);
+    cudaDeviceSynchronize();
+  }
   for (auto& kv : ctx.programs)
     if (kv.second->graph) cudaGraphExecDestroy(kv.second->graph);
   ctx.programs.clear();
@@ -1203,6 +1210,7 @@ static std::shared_ptr<Program> build_program(const Plan& plan, Ctx& ctx, const 
 
 static cudaEvent_t event_at(Ctx& ctx, int i) {
   while ((int)ctx.events.size() <= i) {
+    DeviceGuard g(ctx.device);  // events belong to the context's device
     cudaEvent_t e;
     CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     ctx.events.push_back(e);

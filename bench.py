@@ -307,6 +307,28 @@ def main():
         rt, den = t[0].item(), t[1].item()
     rt_err = math.sqrt(rt / den)
 
+    # the reference bench's protocol (bench.cpp:300-339): each
+    # rep times fwd and inv separately with CUDA events after a barrier, max
+    # over ranks, then min and median over the reps
+    reps = []
+    for _ in range(10):
+        barrier()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        ev[0].record(stream)
+        D.execute(fwd, x, ctx, out=y, sync=False)
+        ev[1].record(stream)
+        D.execute(bwd, y, ctx, out=z, sync=False)
+        ev[2].record(stream)
+        torch.cuda.synchronize()
+        reps.append((max_over_ranks(ev[0].elapsed_time(ev[1])), max_over_ranks(ev[1].elapsed_time(ev[2]))))
+
+    def minmed(v):
+        v = sorted(v)
+        return {"min": v[0], "median": v[(len(v) - 1) // 2]}
+
+    ref_protocol = {"reps": len(reps), "fwd_ms": minmed([a for a, _ in reps]),
+                    "inv_ms": minmed([b for _, b in reps]), "fwdinv_ms": minmed([a + b for a, b in reps])}
+
     # per-pass device times: CUDA events around every pass / sync point of 3
     # more steps (op by op, no graph), TimingBreakdown + ExecContext.last_ops
     tb_f, tb_b = D.TimingBreakdown(), D.TimingBreakdown()
@@ -459,6 +481,7 @@ def main():
                                  "total": tb_f.total / 3 * 1e3},
             "step_ops_ms": {"passes": pass_ms, "exchange_passes": exch_ms, "sync_points": sync_ms},
             "ops_one_step": op_list,
+            "reference_protocol": ref_protocol,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -1349,10 +1349,21 @@ static void run_timed(Ctx& ctx, Program& pr, cudaStream_t s, dfftb_timing* timer
     cudaEvent_t a, b;
     const Op* op;
   };
+  // every event created here is destroyed on every exit path
+  struct Events {
+    std::vector<cudaEvent_t> all;
+    ~Events() {
+      for (auto e : all) cudaEventDestroy(e);
+    }
+    cudaEvent_t make() {
+      cudaEvent_t e = nullptr;
+      CUDA_TRY(cudaEventCreate(&e));
+      all.push_back(e);
+      return e;
+    }
+  } evs;
   std::vector<Mark> marks;
-  cudaEvent_t t0, t1;
-  CUDA_TRY(cudaEventCreate(&t0));
-  CUDA_TRY(cudaEventCreate(&t1));
+  cudaEvent_t t0 = evs.make(), t1 = evs.make();
   CUDA_TRY(cudaEventRecord(t0, s));
   fork_side(ctx, pr, s);
   for (const auto& op : pr.ops) {
@@ -1360,8 +1371,8 @@ static void run_timed(Ctx& ctx, Program& pr, cudaStream_t s, dfftb_timing* timer
     cudaStream_t st = op.stream ? static_cast<cudaStream_t>(ctx.side) : s;
     Mark m{nullptr, nullptr, &op};
     if (timed) {
-      CUDA_TRY(cudaEventCreate(&m.a));
-      CUDA_TRY(cudaEventCreate(&m.b));
+      m.a = evs.make();
+      m.b = evs.make();
       CUDA_TRY(cudaEventRecord(m.a, st));
     }
     launch_op(ctx, op, s);
@@ -1394,14 +1405,10 @@ static void run_timed(Ctx& ctx, Program& pr, cudaStream_t s, dfftb_timing* timer
       timers->local_fft += sec;
     }
     ctx.last_ops.push_back(ot);
-    cudaEventDestroy(m.a);
-    cudaEventDestroy(m.b);
   }
   float ms = 0;
   cudaEventElapsedTime(&ms, t0, t1);
   timers->total = ms * 1e-3;
-  cudaEventDestroy(t0);
-  cudaEventDestroy(t1);
   if (knobs().op_times) {
     static const char* kinds[3] = {"local", "exchange", "sync"};
     for (const auto& o : ctx.last_ops)

@@ -339,14 +339,30 @@ def main():
         D.execute(bwd, y, ctx, out=z, timers=tb_b)
         ops += [("bwd",) + o for o in ctx.last_ops()]
     pass_ms = sum(o[4] for o in ops if o[1] != "sync") / 3  # per step, all passes
+    local_ms = sum(o[4] for o in ops if o[1] == "local") / 3
     exch_ms = sum(o[4] for o in ops if o[1] == "exchange") / 3
     sync_ms = sum(o[4] for o in ops if o[1] == "sync") / 3
-    passes = 6  # logical passes per fwd+inv (chunks of one pass count once)
-    avg_pass_ms = max_over_ranks(pass_ms / passes)
+    n_local = sum(1 for o in ops if o[1] == "local") // 3
     local_elems = fwd.input.local_count(rank)
     alg_bytes = 2 * 16 * local_elems  # one read + one write of the local block per pass
     peak, peak_kind = peaks()
+    # HBM roofline of the dominant HBM-bound kernel: the local passes (all 6
+    # passes at N=1; the exchange passes are NVLink-bound and reported below)
+    avg_pass_ms = max_over_ranks(local_ms / max(1, n_local))
     achieved = alg_bytes / (avg_pass_ms * 1e-3) / 1e9
+    # NVLink: payload each rank stores into OTHER ranks per step (the plans'
+    # exchange counts, make_transpose_step) over the exchange passes' time
+    # pencil transposes (plan.hpp:149-236): forward T1 (grid axis 1) then T0
+    # (axis 0), backward T0 then T1; a rank's own section is its coordinate
+    coords = (rank // grid[1], rank % grid[1])
+    remote = 0
+    for plan, axes in ((fwd, (1, 0)), (bwd, (0, 1))):
+        for t in range(plan.transpose_stage_count()):
+            send, _ = plan.exchange_counts(rank, t)
+            if len(send) > 1:
+                remote += 16 * (sum(send) - send[coords[axes[t]]])
+    exch_ms_max = max_over_ranks(exch_ms)
+    nvl_achieved = remote / (exch_ms_max * 1e-3) / 1e9 if exch_ms_max > 0 else None
     op_list = [{"dir": o[0], "kind": o[1], "side_stream": bool(o[2]), "n": o[3], "ms": round(o[4], 4)}
                for o in ops[:len(ops) // 3]]
 
@@ -459,8 +475,16 @@ def main():
                          "frac": achieved / peak, "traffic": traffic,
                          "traffic_source": traffic_src,
                          "algorithmic_bytes_per_pass": alg_bytes,
-                         "kernel": "fft_pass_tma_kernel (average over the 6 passes per fwd+inv; "
-                                   "CUDA events around each pass, 3 steps after the timed region)",
+                         "kernel": "fft_pass_tma_kernel, local passes (average over the %d local passes "
+                                   "per fwd+inv; CUDA events around each pass, 3 steps after the timed "
+                                   "region)" % n_local,
+                         "nvlink": None if nvl_achieved is None else {
+                             "kernel": "fft_pass_tma_kernel, exchange passes (FFT + peer stores)",
+                             "payload_bytes_per_step": remote, "exchange_ms_per_step": exch_ms_max,
+                             "achieved": nvl_achieved, "unit": "GB/s",
+                             "peak_measured": NVL_MEASURED_GBS, "frac_measured": nvl_achieved / NVL_MEASURED_GBS,
+                             "peak_nominal": NVL_NOMINAL_GBS, "frac_nominal": nvl_achieved / NVL_NOMINAL_GBS,
+                             "counters": "profiles/r2/ncu_nvlink_exchange_pass_summary.txt (ncu nvltx bytes)"},
                          "peak_source": peak_kind,
                          "step_bound": "nvlink" if t_nvl > t_hbm else "hbm",
                          "step_roofline_ms": 1e3 * max(t_hbm, t_nvl),

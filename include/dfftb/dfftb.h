@@ -61,11 +61,17 @@ enum { DFFTB_FORWARD = 0, DFFTB_BACKWARD = 1 };
 enum { DFFTB_SLAB = 0, DFFTB_PENCIL = 1, DFFTB_GENERAL = 2 };
 /* template parameter T: bytes per real component */
 enum { DFFTB_F32 = 4, DFFTB_F64 = 8 };
-/* ExchangePath (exchange.hpp:425).  On B200 all three are the fused FFT +
- * peer-memory exchange with byte-identical results, as in the reference.
- * PIPELINED with chunks_per_peer = C > 1 additionally chunks every exchange
- * pass that feeds a local pass into C pieces overlapped with that pass on a
- * second stream (pipelined_all_to_all, exchange.hpp:323-423). */
+/* ExchangePath (exchange.hpp:425).  All three give byte-identical results,
+ * as in the reference.  BLOCKING and STAGED (the staging hop of
+ * exchange.hpp:225-246): an exchange pass that feeds a local pass stores the
+ * other members' parts into local staging images, and copy-engine DMAs move
+ * them over NVLink chunk by chunk (chunks_per_peer > 1, else 8) while the
+ * SMs run the following local pass; any other exchange pass stores every
+ * member's part straight into its buffer over NVLink (all of them with the
+ * environment variable DFFTB_DMA=0).  PIPELINED with chunks_per_peer = C > 1
+ * instead chunks such an exchange pass into C pieces overlapped with the
+ * local pass on a second stream and a share of the SMs
+ * (pipelined_all_to_all, exchange.hpp:323-423). */
 enum { DFFTB_EXCHANGE_BLOCKING = 0, DFFTB_EXCHANGE_STAGED = 1, DFFTB_EXCHANGE_PIPELINED = 2 };
 /* plan layout sides */
 enum { DFFTB_INPUT = 0, DFFTB_OUTPUT = 1 };
@@ -74,7 +80,7 @@ enum { DFFTB_INPUT = 0, DFFTB_OUTPUT = 1 };
 typedef struct {
   int exchange;        /* DFFTB_EXCHANGE_* */
   int normalize;       /* backward applies 1/N once (default 1) */
-  int chunks_per_peer; /* >= 1; PIPELINED: chunks of the overlapped exchange */
+  int chunks_per_peer; /* >= 1; chunks of the overlapped exchange (staged / pipelined) */
   int staging_buffers; /* >= 1; no staging copies exist on B200 (accepted) */
   int validate_finite; /* reject NaN/Inf input (ConfigInvalid, reported after
                           the launches so the ranks stay in lockstep) */
@@ -207,10 +213,15 @@ const char* dfftb_last_error_message(void);
 
 /* Per-op device times of the last execute that was given `timers`, in
  * program order: kinds[i] 0 = local FFT pass, 1 = exchange pass (FFT whose
- * stores go to other ranks' buffers), 2 = sync point; streams[i] 1 = the
- * overlapped pass on the context's side stream; lengths[i] = the transform
- * length.  Returns the op count (arrays filled up to `max`). */
-int dfftb_ctx_last_ops(dfftb_ctx ctx, int* kinds, int* streams, int* lengths, double* ms, int max);
+ * stores go to other ranks' buffers or their staging images), 2 = sync
+ * point, 3 = copy-engine DMA of the staged exchange; streams[i] 1 = the
+ * overlapped pass on the context's side stream, 2 = its copy streams;
+ * lengths[i] = the transform length; shares[i] = the fraction of the pass's
+ * lanes a (chunked) pass launch covers; starts[i] = ms from the start of the
+ * execute.  Any array may be NULL.  Returns the op count (arrays filled up
+ * to `max`). */
+int dfftb_ctx_last_ops(dfftb_ctx ctx, int* kinds, int* streams, int* lengths, double* shares, double* starts,
+                       double* ms, int max);
 
 /* Number of dfftb kernels launched by this process so far (evidence counter). */
 uint64_t dfftb_kernel_launch_count(void);

@@ -57,7 +57,8 @@ _SIGS = {
     "dfftb_ctx_check": (_c.c_int, [vp, vp]),
     "dfftb_world_create": (_c.c_int, [vp, _c.c_int, _c.POINTER(vp)]),
     "dfftb_world_create_devices": (_c.c_int, [vp, _c.c_int, ip, _c.POINTER(vp)]),
-    "dfftb_ctx_last_ops": (_c.c_int, [vp, ip, ip, ip, _c.POINTER(_c.c_double), _c.c_int]),
+    "dfftb_ctx_last_ops": (_c.c_int, [vp, ip, ip, ip, _c.POINTER(_c.c_double), _c.POINTER(_c.c_double),
+                                      _c.POINTER(_c.c_double), _c.c_int]),
     "dfftb_execute_world": (_c.c_int, [vp, _c.POINTER(vp), _c.POINTER(vp), _c.POINTER(vp), vp,
                                        _c.c_int]),
     "dfftb_fill_seeded": (_c.c_int, [vp, _c.c_int, _c.c_int, _c.c_uint64, _c.c_int, vp, vp]),

@@ -247,8 +247,9 @@ dfftb_status dfftb_world_create_devices(dfftb_plan plan, int ndevices, const int
   });
 }
 
-int dfftb_ctx_last_ops(dfftb_ctx ctx, int* kinds, int* streams, int* lengths, double* ms, int max) {
-  return ctx ? dfftb::last_op_times(*ctx->ctx, kinds, streams, lengths, ms, max) : 0;
+int dfftb_ctx_last_ops(dfftb_ctx ctx, int* kinds, int* streams, int* lengths, double* shares, double* starts,
+                       double* ms, int max) {
+  return ctx ? dfftb::last_op_times(*ctx->ctx, kinds, streams, lengths, shares, starts, ms, max) : 0;
 }
 
 dfftb_status dfftb_execute_world(dfftb_plan plan, dfftb_ctx* ctxs, const void* const* d_in,

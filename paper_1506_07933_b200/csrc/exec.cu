@@ -14,13 +14,15 @@
 //   FFT followed by a local FFT  -> private work buffer
 // so each axis costs one read + one write of the local block.
 //
-// Overlap (pipelined_all_to_all, exchange.hpp:323-423).  An
-// exchange pass followed by a local pass is split into chunks along the lane
-// axis both passes share: the exchange pass runs chunk after chunk on the
-// caller's stream and signals each finished chunk to its group; the local
-// pass runs on a side stream, on the other SMs, and starts chunk c as soon as
-// every group member has signalled it -- the NVLink-bound pass and the
-// HBM-bound pass run concurrently instead of back to back.
+// Overlap.  An exchange pass followed by a local pass is
+// split into chunks along the lane axis both passes share.  Default (staged,
+// exchange.hpp:225-246): the exchange pass writes the other members' parts
+// into local staging images at HBM speed, copy-engine DMAs stream chunk c
+// over NVLink and signal it, and the local pass starts chunk c as soon as
+// every member's chunk c has landed -- NVLink traffic runs under the SM
+// passes.  PIPELINED (pipelined_all_to_all, exchange.hpp:323-423): the
+// exchange pass stores to the peers itself, chunk by chunk, on a share of
+// the SMs while the local pass runs on the others.
 //
 // Programs are lowered once per (plan, buffers, parity) and cached in the
 // context; the launches of a cached program are captured into a CUDA graph.
@@ -76,6 +78,14 @@ struct Knobs {
                               // 512^3 4.18 -> 4.14 ms, but 1024^3 46.4 -> 53.4 ms)
   bool rhalf = true;          // DFFTB_RHALF: R2C / C2R lanes as half-length complex FFTs
   int row_align = 32;         // DFFTB_ROW_ALIGN: internal row padding in bytes (16, 32 or 64)
+  bool dma_flat = true;       // DFFTB_DMA_FLAT: staged exchanges keep the [x0][x1][x2] order (2-D boxes)
+  int dma_streams = 2;        // DFFTB_DMA_STREAMS: copy streams of the staged exchange (1..4; chunks
+                              // round-robin, so up to that many DMAs in flight)
+  int dma = 1;                // DFFTB_DMA: staged copy-engine exchange for Blocking / Staged plans
+                              // (0: direct peer stores everywhere)
+  int dma_chunks = 8;         // DFFTB_DMA_CHUNKS: chunks of a staged exchange (chunks_per_peer > 1 wins)
+  double dma_min_mb = 128.0;  // DFFTB_DMA_MIN_MB: smallest block per rank (MiB) worth staging
+  int dma_min_row = 1024;     // DFFTB_DMA_MIN_ROW: smallest chunk row (bytes) worth staging
 };
 
 static const Knobs& knobs() {
@@ -97,6 +107,12 @@ static const Knobs& knobs() {
     k.op_times = flag("DFFTB_OP_TIMES", false);
     k.pdl = flag("DFFTB_PDL", false);
     k.rhalf = flag("DFFTB_RHALF", true);
+    if (const char* e = getenv("DFFTB_DMA")) k.dma = atoi(e);
+    if (const char* e = getenv("DFFTB_DMA_CHUNKS")) k.dma_chunks = std::max(1, std::min(16, atoi(e)));
+    if (const char* e = getenv("DFFTB_DMA_MIN_MB")) k.dma_min_mb = atof(e);
+    if (const char* e = getenv("DFFTB_DMA_MIN_ROW")) k.dma_min_row = atoi(e);
+    k.dma_flat = flag("DFFTB_DMA_FLAT", true);
+    if (const char* e = getenv("DFFTB_DMA_STREAMS")) k.dma_streams = std::max(1, std::min(kCopyStreams, atoi(e)));
     if (const char* e = getenv("DFFTB_ROW_ALIGN")) {
       const int a = atoi(e);
       k.row_align = (a == 16 || a == 32 || a == 64 || a == 128) ? a : 32;
@@ -342,10 +358,20 @@ static size_t table_bytes(const Plan& plan) {
   return t;
 }
 
+// Region granularity.  With peers, the exchange buffers start on 2 MiB
+// boundaries: NVLink writes into a buffer 32 KiB off a 2 MiB page run at
+// 554 instead of 770 GB/s (copy engine, both directions;
+// profiles/r2/ce_ipc_probe.txt).
+static size_t region_align(const Plan& plan) { return plan.nranks() > 1 ? (size_t)2 << 20 : 256; }
+static size_t round_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+static size_t staging_bytes(const Plan& plan, size_t blk);
+
 size_t workspace_bytes(const Plan& plan, int rank) {
   if (rank < 0 || rank >= plan.nranks()) raise(DFFTB_InvalidRank, "rank out of range");
-  const size_t blk = (family_bytes(plan) + 255) / 256 * 256;
-  return kFlagsBytes + (size_t)family_parities(plan) * family_exch_slots(plan) * blk +
+  const size_t al = region_align(plan);
+  const size_t blk = round_up(family_bytes(plan), al);
+  return round_up(kFlagsBytes, al) + (size_t)family_parities(plan) * family_exch_slots(plan) * blk +
+         staging_bytes(plan, blk) +
          (family_needs_work(plan) ? blk : 0) + kStatWords * sizeof(unsigned long long) + table_bytes(plan);
 }
 
@@ -363,15 +389,18 @@ Ctx* ctx_create(const Plan& plan, int rank, int device) {
   ctx->grid = plan.grid;
   ctx->decomp = plan.decomp;
   ctx->kind_family = plan.kind == DFFTB_C2C ? 0 : 1;
-  const size_t blk = (family_bytes(plan) + 255) / 256 * 256;
-  ctx->flags_bytes = kFlagsBytes;
+  const size_t al = region_align(plan);
+  const size_t blk = round_up(family_bytes(plan), al);
+  ctx->flags_bytes = round_up(kFlagsBytes, al);
   ctx->exch_bytes = blk;
   ctx->exch_slots = family_exch_slots(plan);
   ctx->parities = family_parities(plan);
-  ctx->region_bytes = kFlagsBytes + (size_t)ctx->parities * ctx->exch_slots * blk;  // [slot][parity] buffers
+  ctx->region_bytes = ctx->flags_bytes + (size_t)ctx->parities * ctx->exch_slots * blk;  // [slot][parity] buffers
   ctx->work_bytes = family_needs_work(plan) ? blk : 0;
   ctx->table_bytes = table_bytes(plan);
   CUDA_TRY(cudaMalloc(&ctx->region, ctx->region_bytes));
+  ctx->staging_bytes = staging_bytes(plan, blk);
+  if (ctx->staging_bytes) CUDA_TRY(cudaMalloc(&ctx->staging, ctx->staging_bytes));
   CUDA_TRY(cudaMemset(ctx->region, 0, kFlagsBytes));
   if (ctx->work_bytes) CUDA_TRY(cudaMalloc(&ctx->work, ctx->work_bytes));
   CUDA_TRY(cudaMalloc(&ctx->dstat, kStatWords * sizeof(unsigned long long)));
@@ -399,9 +428,17 @@ Ctx* ctx_create(const Plan& plan, int rank, int device) {
     }
     ctx->twiddles[n] = upload_complex(w, plan.prec);
   }
-  cudaStream_t side = nullptr, cap = nullptr;
+  cudaStream_t side = nullptr, cap = nullptr, cpy = nullptr;
   CUDA_TRY(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
   CUDA_TRY(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+  {
+    int lo = 0, hi = 0;
+    CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    for (int k = 0; k < kCopyStreams; ++k) {
+      CUDA_TRY(cudaStreamCreateWithPriority(&cpy, cudaStreamNonBlocking, hi));
+      ctx->copies.push_back(cpy);
+    }
+  }
   ctx->side = side;
   ctx->capture = cap;
   ctx->peer_region.assign(ctx->nranks, nullptr);
@@ -451,6 +488,17 @@ void ctx_connect(Ctx& ctx, const CtxHandle* handles) {
       std::memcpy(&ih, h.ipc, sizeof(ih));
       void* p = nullptr;
       CUDA_TRY(cudaIpcOpenMemHandle(&p, ih, cudaIpcMemLazyEnablePeerAccess));
+      // peer access to the owner's device (when this process sees it under
+      // the same ordinal): copy-engine DMAs into the mapping (staged
+      // exchange) take the direct NVLink path only with it
+      int ndev = 0, can = 0;
+      cudaGetDeviceCount(&ndev);
+      if (h.device != ctx.device && h.device >= 0 && h.device < ndev &&
+          cudaDeviceCanAccessPeer(&can, ctx.device, (int)h.device) == cudaSuccess && can) {
+        cudaError_t e = cudaDeviceEnablePeerAccess((int)h.device, 0);
+        (void)e;
+        cudaGetLastError();
+      }
       ctx.peer_region[r] = p;
       ctx.peer_opened[r] = true;
     }
@@ -476,6 +524,8 @@ void ctx_destroy(Ctx* ctx) {
     for (void* e : ctx->events) cudaEventDestroy(static_cast<cudaEvent_t>(e));
     if (ctx->side) cudaStreamDestroy(static_cast<cudaStream_t>(ctx->side));
     if (ctx->capture) cudaStreamDestroy(static_cast<cudaStream_t>(ctx->capture));
+    for (void* c : ctx->copies) cudaStreamDestroy(static_cast<cudaStream_t>(c));
+    cudaFree(ctx->staging);
     cudaFree(ctx->region);
     cudaFree(ctx->work);
     cudaFree(ctx->dstat);
@@ -504,6 +554,13 @@ void world_create(const Plan& plan, const int* devices, int ndev, Ctx** out) {
   }
   for (int r = 0; r < P; ++r) {
     for (int q = 0; q < P; ++q) ctxs[r]->peer_region[q] = ctxs[q]->region;
+    {
+      // lockstep emulation issues no staged exchange
+      DeviceGuard g(ctxs[r]->device);
+      cudaFree(ctxs[r]->staging);
+      ctxs[r]->staging = nullptr;
+      ctxs[r]->staging_bytes = 0;
+    }
     ctxs[r]->world_mode = true;
     ctxs[r]->connected = true;
     out[r] = ctxs[r];
@@ -512,11 +569,23 @@ void world_create(const Plan& plan, const int* devices, int ndev, Ctx** out) {
 
 // ---------------------------------------------------------------- programs
 
-enum class OpKind { Pass, Begin, Sync, Record, WaitEvent };
+enum class OpKind { Pass, Begin, Sync, Record, WaitEvent, Copy };
+
+// One pitched 3-D box copied by the copy engine (staged exchange): the
+// same box of two buffers with the same layout, innermost axis contiguous.
+struct CopyBox {
+  void* src = nullptr;
+  void* dst = nullptr;
+  size_t pitch = 0;      // bytes between rows
+  size_t ysize = 0;      // rows per slice
+  size_t pos[3] = {0, 0, 0};  // x bytes, y rows, z slices
+  size_t ext[3] = {0, 0, 0};
+  bool flat = false;     // full rows per slice: one 2-D copy of ext[1] * ext[2] rows
+};
 
 struct Op {
   OpKind kind = OpKind::Pass;
-  int stream = 0;  // 0 caller's stream, 1 the context's side stream
+  int stream = 0;  // 0 caller's stream, 1 the context's side stream, 2 its copy stream
   // ---- pass
   bool tma = false;
   bool generic = false;  // non-power-of-two length: mixed-radix / Bluestein kernel
@@ -524,6 +593,7 @@ struct Op {
   bool remote = false;   // some destination is another rank's buffer
   int n = 1;
   int grid_sms = 0;      // > 0: persistent grid limited to this many SMs (overlap split)
+  double share = 1.0;    // fraction of the pass's lanes this launch covers (chunks)
   PassParams p{};
   TmaPlan tp{};
   GenParams g{};
@@ -532,6 +602,12 @@ struct Op {
   int u = -1;                // exchange passes: the transpose's gather axis
   const Dist* before = nullptr;
   std::vector<int> members;  // exchange group (world ranks, group order)
+  // exchange passes: this rank's block (before) and every member's target
+  // block extents / element strides (staged exchange boxes)
+  std::array<int64_t, kMaxDims> offb{}, lenb{};
+  std::vector<std::array<int64_t, kMaxDims>> dlen, dstr;
+  // ---- copy
+  CopyBox cp{};
   // ---- sync point / events / begin
   bool signal = false, wait = false;
   int slot = 0;
@@ -874,6 +950,8 @@ static bool lower_single(const Plan& plan, const Ctx& ctx, const void* d_in, voi
 }
 
 // One rank's program: fused passes and sync points, in stage order.
+static bool staged_applies(const Plan& plan, const Ctx& ctx);
+
 static std::vector<Op> lower(const Plan& plan, const Ctx& ctx, const void* d_in, void* d_out, int parity) {
   std::vector<Op> prog;
   if (lower_single(plan, ctx, d_in, d_out, parity, prog)) return prog;
@@ -941,17 +1019,27 @@ static std::vector<Op> lower(const Plan& plan, const Ctx& ctx, const void* d_in,
       const int u = tr->before.axis_of_grid[g];
       // the transposed final forward exchange feeds the axis-0 pass: store
       // its buffer [x1][x0][rest] so axis-0 lanes read short strides
-      const bool swap_out = tr->transposed && knobs().zperm && nd >= 3;
+      const bool swap_out = tr->transposed && knobs().zperm && nd >= 3 && !(staged_applies(plan, ctx) && knobs().dma_flat);
       op.u = u;
       op.members = group_members(Lo, me, g);
       op.remote = op.members.size() > 1;
       p.ndest = (int)op.members.size();
       p.oblk = (Lo.dims[v] + Lo.grid[g] - 1) / Lo.grid[g];
+      for (int a = 0; a < nd; ++a) {
+        op.offb[a] = offb[a];
+        op.lenb[a] = lenb[a];
+      }
+      op.dlen.resize(p.ndest);
+      op.dstr.resize(p.ndest);
       for (int q = 0; q < p.ndest; ++q) {
         const int rq = op.members[q];
         int64_t offo[kMaxDims], leno[kMaxDims], so[kMaxDims];
         Lo.extents_of(rq, offo, leno);
         row_major_strides(leno, nd, so, true, ctx.prec, swap_out);
+        for (int a = 0; a < nd; ++a) {
+          op.dlen[q][a] = leno[a];
+          op.dstr[q][a] = so[a];
+        }
         Dest& d = p.dest[q];
         d.ptr = ctx.exch(rq, slot, parity);
         d.base = offb[u] * so[u];
@@ -1114,7 +1202,10 @@ static void overlap_pairs(std::vector<Op>& prog, const Plan& plan, const Ctx& ct
       const int64_t x0 = std::min<int64_t>(Xe, c * R), x1 = std::min<int64_t>(Xe, x0 + R);
       if (p_box || c == 0) {
         Op pc = P;  // without box support the whole pass runs in chunk 0
-        if (p_box) pc.tp.args = chunk_box(P, X, x0, x1, P.tp.args.W);
+        if (p_box) {
+          pc.tp.args = chunk_box(P, X, x0, x1, P.tp.args.W);
+          pc.share = Xe > 0 ? (double)(x1 - x0) / (double)Xe : 0.0;
+        }
         pc.grid_sms = gP;
         if (!p_box || x1 > x0) out.push_back(pc);
       }
@@ -1141,7 +1232,10 @@ static void overlap_pairs(std::vector<Op>& prog, const Plan& plan, const Ctx& ct
       if (q_box || c == C - 1) {
         Op qc = Q;  // without box support the whole pass runs after the last chunk
         qc.stream = 1;
-        if (q_box) qc.tp.args = chunk_box(Q, X, x0, x1, Q.tp.args.W);
+        if (q_box) {
+          qc.tp.args = chunk_box(Q, X, x0, x1, Q.tp.args.W);
+          qc.share = Xe > 0 ? (double)(x1 - x0) / (double)Xe : 0.0;
+        }
         qc.grid_sms = sms - gP;
         if (!q_box || x1 > x0) out.push_back(qc);
       }
@@ -1162,19 +1256,216 @@ static void overlap_pairs(std::vector<Op>& prog, const Plan& plan, const Ctx& ct
   prog.swap(out);
 }
 
-// Sync slots: every barrier gets its own slot; the signal of chunk c and the
-// wait that follows it share one.
+// ---------------------------------------------------------- staged exchange
+//
+// ExchangePath::Staged on the copy engine (or every plan with DFFTB_DMA=1).  The same
+// [P: exchange pass][sync][Q: local pass] triple, in C chunks along the same
+// shared lane axis X as above, becomes
+//   caller's stream: P chunk 0 .. C-1 on every SM, storing the other
+//     members' parts into local staging images of their buffers (same
+//     layout and offsets; pack_into_staging, exchange.hpp) and its own part
+//     into its own buffer -- HBM-speed stores only;  then per chunk c:
+//     wait for sync point k_c, Q chunk c on every SM;
+//   copy stream: per chunk c: wait for P chunk c, copy chunk c's box of
+//     every staging image into that member's buffer (one pitched 3-D DMA
+//     per member over NVLink), signal k_c to the group.
+// No SM ever stalls on NVLink: the copy engine streams chunk c while the SMs
+// run P's later chunks and Q's earlier ones.  The op and sync sequence is
+// rank-independent (C signals and C waits per triple); chunk ranges are
+// multiples of 64 lanes along a tile axis, which every tile width divides.
+
+// staging images: one buffer per other member of the largest exchange group
+static size_t staging_bytes(const Plan& plan, size_t blk) {
+  if (plan.nranks() < 2 || knobs().dma <= 0) return 0;
+  int g = 1;
+  for (int x : plan.grid) g = std::max(g, x);
+  return (size_t)(g - 1) * blk;
+}
+
+static bool staged_applies(const Plan& plan, const Ctx& ctx) {
+  return knobs().dma > 0 && plan.options.exchange != DFFTB_EXCHANGE_PIPELINED && !ctx.world_mode &&
+         ctx.nranks > 1 && plan.nranks() > 1 && ctx.staging != nullptr;
+}
+
+// chunk c's box of member q's buffer written by this rank's exchange pass
+static bool staged_box(const Op& P, int q, int X, int64_t x0, int64_t x1, int csize, CopyBox& cb) {
+  int64_t lo[3], hi[3];
+  for (int a = 0; a < 3; ++a) {
+    if (a == P.u) {
+      lo[a] = P.offb[a];
+      hi[a] = P.offb[a] + P.lenb[a];
+    } else if (a == P.v) {
+      lo[a] = 0;
+      hi[a] = P.dlen[q][a];
+    } else {
+      lo[a] = x0;
+      hi[a] = x1;
+    }
+    if (hi[a] <= lo[a]) return false;
+  }
+  (void)X;
+  int ord[3] = {0, 1, 2};  // D, H, W: strides descending
+  std::sort(ord, ord + 3, [&](int a, int b) { return P.dstr[q][a] > P.dstr[q][b]; });
+  const int D = ord[0], H = ord[1], W = ord[2];
+  const auto& st = P.dstr[q];
+  if (st[W] != 1 || st[H] < P.dlen[q][W] || st[D] % st[H] != 0) raise(DFFTB_Unsupported, "staged box layout");
+  cb.pitch = (size_t)st[H] * csize;
+  cb.ysize = (size_t)(st[D] / st[H]);
+  cb.pos[0] = (size_t)lo[W] * csize;
+  cb.pos[1] = (size_t)lo[H];
+  cb.pos[2] = (size_t)lo[D];
+  cb.ext[0] = (size_t)(hi[W] - lo[W]) * csize;
+  cb.ext[1] = (size_t)(hi[H] - lo[H]);
+  cb.ext[2] = (size_t)(hi[D] - lo[D]);
+  cb.flat = cb.ext[1] == cb.ysize || cb.ext[2] == 1;
+  return true;
+}
+
+static void staged_pairs(std::vector<Op>& prog, const Plan& plan, const Ctx& ctx, int& nevents) {
+  if (!staged_applies(plan, ctx)) return;
+  int C = knobs().dma_chunks;
+  if (plan.options.chunks_per_peer > 1) C = std::min(16, plan.options.chunks_per_peer);
+  C = std::max(1, C);
+  const int me = ctx.rank;
+  const int csize = 2 * ctx.prec;
+  std::vector<Op> out;
+  size_t i = 0;
+  while (i < prog.size()) {
+    bool pattern = i + 2 < prog.size() && overlap_shape(prog[i]) && prog[i].remote &&
+                   prog[i + 1].kind == OpKind::Sync && overlap_shape(prog[i + 2]) && !prog[i + 2].remote &&
+                   prog[i + 2].p.ndest == 1;
+    const int X = pattern ? 3 - prog[i].v - prog[i + 2].v : -1;
+    pattern = pattern && prog[i].v != prog[i + 2].v && X >= 0 && X < 3 && X != prog[i].u &&
+              (X == prog[i].ax_a || X == prog[i].ax_b) && (X == prog[i + 2].ax_a || X == prog[i + 2].ax_b);
+    if (pattern) {
+      // worth it?  DMA launches cost microseconds and short rows slow the
+      // copy engine: stage only big blocks whose chunk rows stay long.
+      // Decided from global sizes only (every rank must agree).
+      const Dist& B = *prog[i].before;
+      double elems = 1.0;
+      for (auto d : B.dims) elems *= (double)d;
+      const double per_rank = elems * csize / (double)plan.nranks();
+      const int gx = B.grid_axis_of(X);
+      const int64_t Xg = gx < 0 ? B.dims[X] : (B.dims[X] + B.grid[gx] - 1) / B.grid[gx];
+      const bool x_inner = X == B.ndim() - 1;  // receiver rows are X-chunks
+      const int64_t u = (X == prog[i].ax_b || X == prog[i + 2].ax_b) ? 64 : 1;
+      const int64_t Rg = ((Xg + C - 1) / C + u - 1) / u * u;
+      pattern = per_rank >= knobs().dma_min_mb * 1048576.0 && (!x_inner || Rg * csize >= knobs().dma_min_row);
+    }
+    if (!pattern) {
+      out.push_back(prog[i++]);
+      continue;
+    }
+    const Op& P = prog[i];
+    const Op& S = prog[i + 1];
+    const Op& Q = prog[i + 2];
+    int64_t offQ[kMaxDims], lenQ[kMaxDims];
+    Q.before->extents_of(me, offQ, lenQ);
+    const int64_t Xe = lenQ[X];
+    const bool p_box = P.tma && !P.generic && (X != P.ax_b || 64 % P.tp.args.W == 0);
+    const bool q_box = Q.tma && !Q.generic && (X != Q.ax_b || 64 % Q.tp.args.W == 0);
+    const int64_t unit = (X == P.ax_b || X == Q.ax_b) ? 64 : 1;
+    const int64_t R = std::max<int64_t>(1, ((Xe + C - 1) / C + unit - 1) / unit * unit);
+    // P with the other members' destinations redirected to staging images
+    Op Ps = P;
+    std::vector<void*> image(P.members.size(), nullptr);
+    {
+      int m = 0;
+      for (size_t q = 0; q < P.members.size(); ++q) {
+        if (P.members[q] == me) continue;
+        image[q] = static_cast<char*>(ctx.staging) + (size_t)m++ * ctx.exch_bytes;
+        Ps.p.dest[q].ptr = image[q];
+      }
+    }
+    const int ncs = knobs().dma_streams;
+    for (int c = 0; c < C; ++c) {
+      const int64_t x0 = std::min<int64_t>(Xe, c * R), x1 = std::min<int64_t>(Xe, x0 + R);
+      const int cs = 2 + c % ncs;  // copy stream of chunk c
+      if (p_box || c == 0) {
+        Op pc = Ps;  // without box support the whole pass runs in chunk 0
+        if (p_box) {
+          pc.tp.args = chunk_box(Ps, X, x0, x1, Ps.tp.args.W);
+          pc.share = Xe > 0 ? (double)(x1 - x0) / (double)Xe : 0.0;
+        }
+        if (!p_box || x1 > x0) out.push_back(pc);
+      }
+      Op rec;
+      rec.kind = OpKind::Record;
+      rec.event = nevents + c;
+      out.push_back(rec);
+      Op we;
+      we.kind = OpKind::WaitEvent;
+      we.stream = cs;
+      we.event = nevents + c;
+      out.push_back(we);
+      for (size_t q = 0; q < P.members.size(); ++q) {
+        if (!image[q]) continue;
+        Op cp;
+        cp.kind = OpKind::Copy;
+        cp.stream = cs;
+        if (!staged_box(P, (int)q, X, x0, x1, csize, cp.cp)) continue;
+        cp.cp.src = image[q];
+        cp.cp.dst = P.p.dest[q].ptr;
+        out.push_back(cp);
+      }
+      Op sig;
+      sig.kind = OpKind::Sync;
+      sig.stream = cs;
+      sig.signal = true;
+      sig.members = S.members;
+      out.push_back(sig);
+    }
+    for (int c = 0; c < C; ++c) {
+      const int64_t x0 = std::min<int64_t>(Xe, c * R), x1 = std::min<int64_t>(Xe, x0 + R);
+      Op wt;
+      wt.kind = OpKind::Sync;
+      wt.wait = true;
+      wt.members = S.members;
+      out.push_back(wt);
+      if (q_box || c == C - 1) {
+        Op qc = Q;  // without box support the whole pass runs after the last chunk
+        if (q_box) {
+          qc.tp.args = chunk_box(Q, X, x0, x1, Q.tp.args.W);
+          qc.share = Xe > 0 ? (double)(x1 - x0) / (double)Xe : 0.0;
+        }
+        if (!q_box || x1 > x0) out.push_back(qc);
+      }
+    }
+    // join: the caller's stream waits for the copy streams (the staging
+    // images are rewritten by the next exchange pass)
+    for (int k = 0; k < ncs; ++k) {
+      Op rj;
+      rj.kind = OpKind::Record;
+      rj.stream = 2 + k;
+      rj.event = nevents + C + k;
+      out.push_back(rj);
+      Op wj;
+      wj.kind = OpKind::WaitEvent;
+      wj.event = nevents + C + k;
+      out.push_back(wj);
+    }
+    nevents += C + ncs;
+    i += 3;
+  }
+  prog.swap(out);
+}
+
+// Sync slots: every barrier gets its own slot; a signal-only point and the
+// wait-only point that consumes it share one (first in, first out).
 static void assign_slots(std::vector<Op>& prog) {
-  int next = 0, open_signal = -1;
+  int next = 0;
+  std::vector<int> open;
+  size_t head = 0;
   for (auto& o : prog) {
     if (o.kind != OpKind::Sync) continue;
     if (o.signal && o.wait) {
       o.slot = next++;
     } else if (o.signal) {
       o.slot = next++;
-      open_signal = o.slot;
+      open.push_back(o.slot);
     } else {
-      o.slot = open_signal;
+      if (head >= open.size()) raise(DFFTB_ConfigInvalid, "sync wait without a signal");
+      o.slot = open[head++];
     }
   }
   if (next > kSyncSlots) raise(DFFTB_Unsupported, "too many sync points in one program");
@@ -1190,13 +1481,16 @@ static std::shared_ptr<Program> build_program(const Plan& plan, Ctx& ctx, const 
                                               int parity, bool allow_overlap = true) {
   auto pr = std::make_shared<Program>();
   std::vector<Op> ops = lower(plan, ctx, d_in, d_out, parity);
-  if (allow_overlap) overlap_pairs(ops, plan, ctx, pr->nevents);
+  if (allow_overlap) {
+    staged_pairs(ops, plan, ctx, pr->nevents);
+    overlap_pairs(ops, plan, ctx, pr->nevents);
+  }
   assign_slots(ops);
   pr->c2r = plan_has_c2r(plan);
   bool has_sync = false;
   for (const auto& o : ops) {
     has_sync = has_sync || o.kind == OpKind::Sync;
-    pr->multi_stream = pr->multi_stream || o.stream != 0;
+    pr->multi_stream = pr->multi_stream || o.stream == 1;
   }
   if (pr->c2r || (has_sync && !ctx.world_mode)) {
     Op b;
@@ -1236,10 +1530,35 @@ static SyncParams sync_params(const Ctx& ctx, const Op& op) {
   return sp;
 }
 
+static cudaStream_t op_stream(const Ctx& ctx, const Op& op, cudaStream_t s) {
+  if (op.stream == 1) return static_cast<cudaStream_t>(ctx.side);
+  if (op.stream >= 2) return static_cast<cudaStream_t>(ctx.copies[op.stream - 2]);
+  return s;
+}
+
 // Issue one op.  `s` = the caller's stream (or the capture stream).
 static void launch_op(Ctx& ctx, const Op& op, cudaStream_t s) {
-  cudaStream_t st = op.stream ? static_cast<cudaStream_t>(ctx.side) : s;
+  cudaStream_t st = op_stream(ctx, op, s);
   switch (op.kind) {
+    case OpKind::Copy: {
+      if (op.cp.flat) {
+        // whole slices (or one slice): one pitched 2-D DMA
+        const size_t off = (op.cp.pos[2] * op.cp.ysize + op.cp.pos[1]) * op.cp.pitch + op.cp.pos[0];
+        CUDA_TRY(cudaMemcpy2DAsync(static_cast<char*>(op.cp.dst) + off, op.cp.pitch,
+                                   static_cast<const char*>(op.cp.src) + off, op.cp.pitch, op.cp.ext[0],
+                                   op.cp.ext[1] * op.cp.ext[2], cudaMemcpyDefault, st));
+        return;
+      }
+      cudaMemcpy3DParms m{};
+      m.srcPtr = make_cudaPitchedPtr(op.cp.src, op.cp.pitch, op.cp.pitch, op.cp.ysize);
+      m.dstPtr = make_cudaPitchedPtr(op.cp.dst, op.cp.pitch, op.cp.pitch, op.cp.ysize);
+      m.srcPos = make_cudaPos(op.cp.pos[0], op.cp.pos[1], op.cp.pos[2]);
+      m.dstPos = m.srcPos;
+      m.extent = make_cudaExtent(op.cp.ext[0], op.cp.ext[1], op.cp.ext[2]);
+      m.kind = cudaMemcpyDefault;
+      CUDA_TRY(cudaMemcpy3DAsync(&m, st));
+      return;
+    }
     case OpKind::Begin:
       CUDA_TRY(launch_sync_begin(ctx.dstat + kStatEpoch, op.herm ? ctx.dstat : nullptr, st));
       return;
@@ -1367,8 +1686,9 @@ static void run_timed(Ctx& ctx, Program& pr, cudaStream_t s, dfftb_timing* timer
   CUDA_TRY(cudaEventRecord(t0, s));
   fork_side(ctx, pr, s);
   for (const auto& op : pr.ops) {
-    const bool timed = op.kind == OpKind::Pass || (op.kind == OpKind::Sync && !ctx.world_mode);
-    cudaStream_t st = op.stream ? static_cast<cudaStream_t>(ctx.side) : s;
+    const bool timed =
+        op.kind == OpKind::Pass || op.kind == OpKind::Copy || (op.kind == OpKind::Sync && !ctx.world_mode);
+    cudaStream_t st = op_stream(ctx, op, s);
     Mark m{nullptr, nullptr, &op};
     if (timed) {
       m.a = evs.make();
@@ -1390,10 +1710,17 @@ static void run_timed(Ctx& ctx, Program& pr, cudaStream_t s, dfftb_timing* timer
     cudaEventElapsedTime(&ms, m.a, m.b);
     const double sec = ms * 1e-3;
     OpTime ot{};
-    ot.stream = m.op->stream;
+    ot.stream = std::min(m.op->stream, 2);
     ot.ms = ms;
+    float st0 = 0;
+    cudaEventElapsedTime(&st0, t0, m.a);
+    ot.start = st0;
+    ot.share = m.op->kind == OpKind::Pass ? m.op->share : 0.0;
     if (m.op->kind == OpKind::Sync) {
       ot.kind = 2;
+      timers->wire_comm += sec;
+    } else if (m.op->kind == OpKind::Copy) {
+      ot.kind = 3;
       timers->wire_comm += sec;
     } else if (m.op->remote) {
       ot.kind = 1;
@@ -1410,9 +1737,10 @@ static void run_timed(Ctx& ctx, Program& pr, cudaStream_t s, dfftb_timing* timer
   cudaEventElapsedTime(&ms, t0, t1);
   timers->total = ms * 1e-3;
   if (knobs().op_times) {
-    static const char* kinds[3] = {"local", "exchange", "sync"};
+    static const char* kinds[4] = {"local", "exchange", "sync", "copy"};
     for (const auto& o : ctx.last_ops)
-      fprintf(stderr, "[dfftb rank %d] %s%s n=%d: %.3f ms\n", ctx.rank, kinds[o.kind], o.stream ? " (side)" : "",
+      fprintf(stderr, "[dfftb rank %d] %s%s n=%d: %.3f ms\n", ctx.rank, kinds[o.kind],
+              o.stream == 1 ? " (side)" : o.stream >= 2 ? " (copy)" : "",
               o.n, o.ms);
   }
 }
@@ -1590,12 +1918,15 @@ void fill_seeded(const Plan& plan, int rank, int side, uint64_t seed, int comple
   CUDA_TRY(launch_seeded(plan.prec, sp, d_buf, s));
 }
 
-int last_op_times(const Ctx& ctx, int* kinds, int* streams, int* lengths, double* ms, int max) {
+int last_op_times(const Ctx& ctx, int* kinds, int* streams, int* lengths, double* shares, double* starts,
+                  double* ms, int max) {
   const int n = (int)ctx.last_ops.size();
   for (int i = 0; i < n && i < max; ++i) {
     if (kinds) kinds[i] = ctx.last_ops[i].kind;
     if (streams) streams[i] = ctx.last_ops[i].stream;
     if (lengths) lengths[i] = ctx.last_ops[i].n;
+    if (shares) shares[i] = ctx.last_ops[i].share;
+    if (starts) starts[i] = ctx.last_ops[i].start;
     if (ms) ms[i] = ctx.last_ops[i].ms;
   }
   return n;

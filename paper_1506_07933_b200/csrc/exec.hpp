@@ -14,7 +14,8 @@ void ctx_connect(Ctx& ctx, const CtxHandle* handles);
 void ctx_destroy(Ctx* ctx);
 void ctx_check(Ctx& ctx, cudaStream_t s);
 void world_create(const Plan& plan, const int* devices, int ndev, Ctx** out);
-int last_op_times(const Ctx& ctx, int* kinds, int* streams, int* lengths, double* ms, int max);
+int last_op_times(const Ctx& ctx, int* kinds, int* streams, int* lengths, double* shares, double* starts,
+                  double* ms, int max);
 void execute(const Plan& plan, Ctx& ctx, const void* d_in, void* d_out, cudaStream_t s, int flags,
              dfftb_timing* timers);
 void execute_world(const Plan& plan, Ctx** ctxs, const void* const* d_in, void* const* d_out,

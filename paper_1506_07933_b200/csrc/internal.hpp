@@ -27,6 +27,7 @@ struct Error {
 const char* status_name(dfftb_status s);
 
 constexpr int kMaxDims = 4;
+constexpr int kCopyStreams = 4;
 constexpr int kMaxRanks = 64;
 
 // ceil-block partition, layout.hpp:80-92
@@ -112,9 +113,11 @@ struct Program;  // exec.cu: one rank's lowered, cached program
 
 // per-op device time of the last timed execute (dfftb_ctx_last_ops)
 struct OpTime {
-  int kind;    // 0 local pass, 1 exchange pass (remote stores), 2 sync point
-  int stream;  // 0 caller's stream, 1 side stream (overlapped consumer)
-  int n;       // transform length (passes)
+  int kind;      // 0 local pass, 1 exchange pass, 2 sync point, 3 copy-engine DMA
+  int stream;    // 0 caller's stream, 1 side stream (overlapped consumer), 2 copy streams
+  int n;         // transform length (passes)
+  double share;  // passes: fraction of the pass's lanes (chunks < 1)
+  double start;  // ms from the start of the execute
   double ms;
 };
 
@@ -155,6 +158,9 @@ struct Ctx {
   // pass of a pipelined pair) and of graph capture
   void* side = nullptr;     // cudaStream_t
   void* capture = nullptr;  // cudaStream_t
+  std::vector<void*> copies;  // cudaStream_t x kCopyStreams, high priority: staged exchange DMAs + signals
+  void* staging = nullptr;  // staged exchange: images of the other members' buffers (lazy)
+  size_t staging_bytes = 0;
   std::vector<void*> events;  // cudaEvent_t pool, grown on demand
   // cached programs: key (plan id, buffers, parity, epilogue) -> program
   std::map<std::string, std::shared_ptr<Program>> programs;

@@ -414,18 +414,21 @@ class ExecContext:
 
     def last_ops(self):
         """Per-op device times of the last execute given `timers`: a list of
-        (kind, stream, length, ms) with kind "local" (FFT pass), "exchange"
-        (FFT pass storing into other ranks' buffers) or "sync"; stream 1 is
-        the overlapped pass on the context's side stream."""
+        (kind, stream, length, share, start_ms, ms) with kind "local" (FFT
+        pass), "exchange" (FFT pass storing into other ranks' buffers or
+        their staging images), "sync" or "copy" (a copy-engine DMA of the
+        staged exchange); stream 1 is the overlapped pass on the context's
+        side stream, 2 its copy streams; share = the fraction of the pass's
+        lanes a chunked pass launch covers; start_ms from the execute's
+        start."""
         L = _lib.lib()
-        n = L.dfftb_ctx_last_ops(self._h, None, None, None, None, 0)
-        k = (ctypes.c_int * max(n, 1))()
-        st = (ctypes.c_int * max(n, 1))()
-        ln = (ctypes.c_int * max(n, 1))()
-        ms = (ctypes.c_double * max(n, 1))()
-        L.dfftb_ctx_last_ops(self._h, k, st, ln, ms, n)
-        names = ("local", "exchange", "sync")
-        return [(names[k[i]], st[i], ln[i], ms[i]) for i in range(n)]
+        n = L.dfftb_ctx_last_ops(self._h, None, None, None, None, None, None, 0)
+        m = max(n, 1)
+        k, st, ln = (ctypes.c_int * m)(), (ctypes.c_int * m)(), (ctypes.c_int * m)()
+        sh, t0, ms = (ctypes.c_double * m)(), (ctypes.c_double * m)(), (ctypes.c_double * m)()
+        L.dfftb_ctx_last_ops(self._h, k, st, ln, sh, t0, ms, n)
+        names = ("local", "exchange", "sync", "copy")
+        return [(names[k[i]], st[i], ln[i], sh[i], t0[i], ms[i]) for i in range(n)]
 
 
 def _resolve_device(device) -> torch.device:

@@ -195,18 +195,23 @@ def test_workspace_bytes():
     # block of the plan family, + status words + the per-axis twiddle (and
     # Bluestein) tables (+ the half-length table of the last axis of R2C / C2R
     # plans, for the half-length real lanes)
+    # With peers the flag page and the buffers are rounded to 2 MiB (NVLink
+    # destinations on 2 MiB boundaries); a single rank rounds to 256 bytes.
     flags = 64 * 64 * 8
+    MiB2 = 2 << 20
     p = D.plan_pencil((512, 512, 512), (2, 4), D.TransformKind.C2C, D.Direction.Forward)
     blk = 512 ** 3 * 16 // 8
-    assert D.workspace_bytes(p, 0) == flags + 2 * 2 * blk + 64 + 512 * 16
+    # + staging images for the copy-engine exchange: one per other member of
+    # the largest group (3 for the 2x4 grid)
+    assert D.workspace_bytes(p, 0) == MiB2 + 2 * 2 * blk + 3 * blk + 64 + 512 * 16
     one = D.plan_pencil((512, 512, 512), (1, 1), D.TransformKind.C2C, D.Direction.Forward)
     assert D.workspace_bytes(one, 0) == flags + 2 * 512 ** 3 * 16 + 64 + 512 * 16  # 2 slots, 1 parity
     sl = D.plan_slab((64, 64, 64), 4, D.TransformKind.C2C, D.Direction.Forward)
-    blk = 64 ** 3 * 16 // 4
-    assert D.workspace_bytes(sl, 0) == flags + 2 * 2 * blk + blk + 64 + 64 * 16  # slab: + work buffer
+    blk = MiB2  # 64^3 * 16 / 4 = 1 MiB, rounded
+    assert D.workspace_bytes(sl, 0) == MiB2 + 2 * 2 * blk + blk + 3 * blk + 64 + 64 * 16  # slab: + work buffer
     q = D.plan_pencil((1024, 64, 64), (2, 4), D.TransformKind.C2C, D.Direction.Forward)
     blk = 1024 * 64 * 64 * 16 // 8
-    assert D.workspace_bytes(q, 0) == flags + 2 * 2 * blk + 64 + (1024 + 64) * 16
+    assert D.workspace_bytes(q, 0) == MiB2 + 2 * 2 * blk + 3 * blk + 64 + (1024 + 64) * 16
     # R2C: + the n/2-point table of the last axis (half-length real lanes)
     r1 = D.plan_pencil((64, 64, 256), (1, 1), D.TransformKind.R2C, D.Direction.Forward)
     c1 = D.plan_pencil((64, 64, 256), (1, 1), D.TransformKind.C2C, D.Direction.Forward)

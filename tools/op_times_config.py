@@ -32,5 +32,5 @@ for name in ("fwd", "bwd"):
     else:
         z = D.execute(bwd, y, ctx, timers=tb)
     print(f"{name} total {tb.total * 1e3:.3f} ms")
-    for kind, stream, n, ms in ctx.last_ops():
-        print(f"  {kind:8s} n={n:5d} {ms:.3f} ms")
+    for kind, stream, n, share, start, ms in ctx.last_ops():
+        print(f"  {kind:8s} n={n:5d} share {share:.3f} at {start:.3f}: {ms:.3f} ms")

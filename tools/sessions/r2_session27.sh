@@ -1,0 +1,17 @@
+#!/bin/bash
+# round-2 GPU session 27 (2 GPUs): copy-engine box rates; staged exchange with 2-D boxes
+O=gpurun_out/s27
+mkdir -p $O
+TR="python -m torch.distributed.run --nnodes=1 --master-addr 127.0.0.1"
+timeout 120 tools/ce_box_probe > $O/ce_box_probe.log 2>&1
+cat $O/ce_box_probe.log
+timeout 300 env DFFTB_DMA=1 $TR --nproc-per-node 2 --master-port 29681 tests/mgpu_check.py > $O/mgpu2_dma.log 2>&1; echo "exit $?" >> $O/mgpu2_dma.log
+tail -2 $O/mgpu2_dma.log
+for c in 4 2 8; do
+  timeout 200 env DFFTB_DMA=1 DFFTB_OVERLAP_CHUNKS=$c $TR --nproc-per-node 2 --master-port 2968$c bench.py --gpus 2 > $O/bench_n2_dma_c$c.log 2>&1
+done
+timeout 200 env DFFTB_DMA=1 DFFTB_OP_TIMES=1 $TR --nproc-per-node 2 --master-port 29689 bench.py --gpus 2 --steps 3 --warmup 3 > $O/optimes_dma.log 2>&1
+timeout 200 $TR --nproc-per-node 2 --master-port 29682 bench.py --gpus 2 > $O/bench_n2_default.log 2>&1
+for f in $O/bench_n2_*.log; do echo "$f: $(grep -o '"ms_per_step": [0-9.]*' $f | head -1)"; done
+grep "rank 0" $O/optimes_dma.log | head -24
+echo done

@@ -123,6 +123,18 @@ def main():
         for _ in range(3):  # repeated executes exercise buffer parity and barriers
             y = D.execute(fwd, x, ctx)
             z = D.execute(bwd, y, ctx)
+        # which exchange mechanisms ran (per-op kinds of one timed execute
+        # per direction): "copy" = copy-engine DMAs of the staged exchange
+        kinds = set()
+        for plan_, inp in ((fwd, x), (bwd, y)):
+            D.execute(plan_, inp, ctx, timers=D.TimingBreakdown())
+            kinds |= {o[0] for o in ctx.last_ops()}
+        staged_ran = torch.tensor([1 if "copy" in kinds else 0], device=FLAG_DEV)
+        dist.all_reduce(staged_ran, op=dist.ReduceOp.MAX)
+        if os.environ.get("DFFTB_EXPECT_STAGED") == "1" and rank == 0 and staged_ran.item() == 0 and \
+                decomp == "pencil" and kind == "c2c":
+            print(f"FAIL {decomp} {dims} grid {grid}: staging forced but no copy-engine DMA ran", flush=True)
+            ok = False
         torch.cuda.synchronize()
         ctx.check()
         yg = gather_global(fwd.output, y, rank, world)
@@ -135,7 +147,8 @@ def main():
             good = e_f <= TOL[prec] and e_r <= TOL[prec]
             ok = ok and good
             print(f"{'ok  ' if good else 'FAIL'} {decomp} {dims} grid {grid} {kind} {prec}: "
-                  f"fwd vs oracle {e_f:.2e}, round trip {e_r:.2e}", flush=True)
+                  f"fwd vs oracle {e_f:.2e}, round trip {e_r:.2e}"
+                  f"{', staged DMA exchange' if staged_ran.item() else ''}", flush=True)
         # fused spectral epilogue == execute + spectral_apply, on every rank
         spec_ok = fused_spectral_matches(fwd, ctx, x, rank)
         # a different chunking of the overlapped exchange (PlanOptions

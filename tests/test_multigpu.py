@@ -20,13 +20,21 @@ def _ngpus():
         return 0
 
 
+# default: the shipped thresholds (these small cases exchange by direct peer
+# stores); staged: every eligible exchange goes through staging images and
+# copy-engine DMAs (size thresholds off), checked to have run
+MODES = {"default": {}, "staged": {"DFFTB_DMA_MIN_MB": "0", "DFFTB_DMA_MIN_ROW": "0", "DFFTB_EXPECT_STAGED": "1"}}
+
+
+@pytest.mark.parametrize("mode", list(MODES))
 @pytest.mark.parametrize("n", [2, 4, 8])
-def test_multi_gpu_parity(n):
+def test_multi_gpu_parity(n, mode):
     if _ngpus() < n:
         pytest.skip(f"needs {n} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-           "--master-addr", "127.0.0.1", "--master-port", str(29500 + n),
+           "--master-addr", "127.0.0.1", "--master-port", str(29500 + n + (10 if mode != "default" else 0)),
            os.path.join(HERE, "mgpu_check.py")]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    env = dict(os.environ, **MODES[mode])
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
     print(r.stdout[-4000:], r.stderr[-4000:])
     assert r.returncode == 0

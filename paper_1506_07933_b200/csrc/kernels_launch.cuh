@@ -83,14 +83,27 @@ struct TmaCfg {
   // TMA rows instead of 16-32 (fp64 tiles are bounded by shared memory).
   // Half-length real lanes (HALFREAL) switch from N >= 64 so that halving the
   // length doubles the lanes per tile in fp32 too.
-  static constexpr int EPREF = (sizeof(T) == 4 && (N >= 256 || (HALFREAL && N >= 64))) ? 16 : 8;
+  // Long fp64 lanes (N >= DFFTB_F64_E16) run radix-16 stages with 256-thread
+  // CTAs: the same 4 lanes per tile, one shared-memory exchange fewer
+  // (1024 = 16*16*4 instead of 8*8*8*2): the contiguous 1024-point pass
+  // 6.85 -> 6.22 ms, the strided ones unchanged (D 46.1 -> 44.2 ms,
+  // profiles/r2/ab_f64_radix16_s43.txt).  512 threads (8 lanes) would need
+  // 264 KB of shared memory.
+#ifndef DFFTB_F64_E16
+#define DFFTB_F64_E16 1024
+#endif
+#ifndef DFFTB_F64_E16_THREADS
+#define DFFTB_F64_E16_THREADS 256
+#endif
+  static constexpr bool E16 = sizeof(T) == 8 && DFFTB_F64_E16 > 0 && N >= DFFTB_F64_E16;
+  static constexpr int EPREF = (E16 || (sizeof(T) == 4 && (N >= 256 || (HALFREAL && N >= 64)))) ? 16 : 8;
   using SC = Sched<N, EPREF>;
   static constexpr int TPL = SC::TPL;
 #ifndef DFFTB_SMALL_W
 #define DFFTB_SMALL_W 16  // lane cap of short (N <= 64) tiles: more, smaller CTAs (64^3: 32 -> 25 us)
 #endif
-  static constexpr int W0 = (N <= 64 && DFFTB_TMA_THREADS / TPL > DFFTB_SMALL_W) ? DFFTB_SMALL_W
-                                                                                 : DFFTB_TMA_THREADS / TPL;
+  static constexpr int THR = E16 ? DFFTB_F64_E16_THREADS : DFFTB_TMA_THREADS;
+  static constexpr int W0 = (N <= 64 && THR / TPL > DFFTB_SMALL_W) ? DFFTB_SMALL_W : THR / TPL;
   static constexpr int W = W0 < 1 ? 1 : (W0 > 64 ? 64 : W0);
   static constexpr int THREADS = W * TPL;
   static constexpr int MINB = DFFTB_TMA_MINB;

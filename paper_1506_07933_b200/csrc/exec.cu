@@ -81,6 +81,7 @@ struct Knobs {
   bool dma_flat = true;       // DFFTB_DMA_FLAT: staged exchanges keep the [x0][x1][x2] order (2-D boxes)
   int dma_streams = 2;        // DFFTB_DMA_STREAMS: copy streams of the staged exchange (1..4; chunks
                               // round-robin, so up to that many DMAs in flight)
+  bool r2c_order = true;      // DFFTB_R2C_ORDER: single-rank R2C forward as F2, F0, F1
   int dma = 1;                // DFFTB_DMA: staged copy-engine exchange for Blocking / Staged plans
                               // (0: direct peer stores everywhere)
   int dma_chunks = 8;         // DFFTB_DMA_CHUNKS: chunks of a staged exchange (chunks_per_peer > 1 wins)
@@ -108,6 +109,7 @@ static const Knobs& knobs() {
     k.pdl = flag("DFFTB_PDL", false);
     k.rhalf = flag("DFFTB_RHALF", true);
     if (const char* e = getenv("DFFTB_DMA")) k.dma = atoi(e);
+    k.r2c_order = flag("DFFTB_R2C_ORDER", true);
     if (const char* e = getenv("DFFTB_DMA_CHUNKS")) k.dma_chunks = std::max(1, std::min(16, atoi(e)));
     if (const char* e = getenv("DFFTB_DMA_MIN_MB")) k.dma_min_mb = atof(e);
     if (const char* e = getenv("DFFTB_DMA_MIN_ROW")) k.dma_min_row = atoi(e);
@@ -858,7 +860,7 @@ static void plan_generic(Op& op, const Ctx& ctx) {
 // One local pass of a 3-D block: axis v of the buffer `in` (extents len,
 // element strides si) into `out` (strides so over the output extents).
 static Op single_pass(const Ctx& ctx, int v, int n, const int64_t* len, const int64_t* si, const void* in,
-                      void* out, const int64_t* so, int fkind, double scale) {
+                      void* out, const int64_t* so, int fkind, double scale, bool inverse = true) {
   int lanes[2], nl = 0;
   for (int a = 0; a < 3; ++a)
     if (a != v) lanes[nl++] = a;
@@ -880,7 +882,7 @@ static Op single_pass(const Ctx& ctx, int v, int n, const int64_t* len, const in
   p.n_out = fkind == DFFTB_R2C ? n / 2 + 1 : n;
   p.in_mode = fkind == DFFTB_R2C ? kInReal : (fkind == DFFTB_C2R ? kInHermitian : kInComplex);
   p.out_real = fkind == DFFTB_C2R;
-  p.inverse = true;
+  p.inverse = inverse;
   p.scale = scale;
   p.tw = is_pow2(n) ? ctx.twiddles.at(n) : nullptr;
   p.tw2 = is_pow2(n) && n >= 16 && ctx.twiddles.count(n / 2) ? p.tw : nullptr;
@@ -912,18 +914,47 @@ static Op single_pass(const Ctx& ctx, int v, int n, const int64_t* len, const in
 static bool lower_single(const Plan& plan, const Ctx& ctx, const void* d_in, void* d_out, int parity,
                          std::vector<Op>& prog) {
   if (plan.nranks() != 1 || plan.input.ndim() != 3 || !knobs().zperm || !knobs().single_reorder) return false;
-  bool backward = false, c2r = false;
+  bool backward = false, c2r = false, r2c = false;
   double scale = 1.0;
+  const Stage* last_fft = nullptr;
   for (const auto& st : plan.stages) {
     if (st.type == StageType::Fft) {
       backward = st.dir == DFFTB_BACKWARD;
       if (st.fkind == DFFTB_C2R) c2r = true;
-      if (st.fkind == DFFTB_R2C) return false;
+      if (st.fkind == DFFTB_R2C) r2c = true;
+      last_fft = &st;
     } else if (st.type == StageType::Normalize) {
       scale = st.factor;
     }
   }
-  if (!backward) return false;
+  if (r2c && knobs().r2c_order) {
+    // R2C forward, mirror of the C2R backward: F2 (R2C) -> [x1][x0][x2]
+    // buffer -> F0 -> plain buffer -> F1 -> user block.  The last pass writes
+    // the user's odd-length (n/2+1) rows with the wide tiles of the middle
+    // axis instead of the 4-lane tiles of a long axis 0 (2048x512x256 fp32:
+    // 32-byte row pieces off the 32-byte sector grid), and axis 0 writes an
+    // aligned internal buffer.
+    int64_t off[3], lr[3], lc[3];
+    plan.input.extents_of(0, off, lr);
+    plan.output.extents_of(0, off, lc);
+    for (int a = 0; a < 3; ++a)
+      if (lc[a] <= 0 || lr[a] <= 0) return false;
+    const int prec = ctx.prec;
+    void* b1 = ctx.exch(0, 0, parity);
+    void* b2 = ctx.exch(0, 1, parity);
+    int64_t s_real[3], s_plain[3], s_swap[3], s_user[3];
+    row_major_strides(lr, 3, s_real, false, prec);
+    row_major_strides(lc, 3, s_plain, true, prec);
+    row_major_strides(lc, 3, s_swap, true, prec, true);
+    row_major_strides(lc, 3, s_user, false, prec);
+    prog.push_back(single_pass(ctx, 2, (int)lr[2], lr, s_real, d_in, b1, s_swap, DFFTB_R2C, 1.0, false));
+    prog.push_back(single_pass(ctx, 0, (int)lc[0], lc, s_swap, b1, b2, s_plain, DFFTB_C2C, 1.0, false));
+    prog.push_back(single_pass(ctx, 1, (int)lc[1], lc, s_plain, b2, d_out, s_user, DFFTB_C2C, 1.0, false));
+    // spectral epilogue coordinates: the (hatted) layout of the last stage
+    if (last_fft) prog.back().before = &last_fft->before;
+    return true;
+  }
+  if (r2c || !backward) return false;
   int64_t off[3], lc[3], lr[3];
   plan.input.extents_of(0, off, lc);   // complex (Hermitian for C2R) extents
   plan.output.extents_of(0, off, lr);  // output extents

@@ -46,7 +46,8 @@
 #define DFFTB_TWB 1  // twiddle bases kept in registers across tiles
 #endif
 #ifndef DFFTB_LS_FP32
-#define DFFTB_LS_FP32 0  // A/B: the bank-aware lane-stride residue for fp32 narrow tiles too
+#define DFFTB_LS_FP32 1  // the bank-aware lane-stride residue for fp32 narrow tiles too (E's
+                         // 2048-point passes: 104 M bank conflicts -> 0.1 M, 0.82 -> 0.73 ms)
 #endif
 #ifndef DFFTB_TMA_MINB
 #define DFFTB_TMA_MINB 1    // resident CTAs per SM the TMA kernel is compiled for
@@ -296,8 +297,8 @@ __host__ __device__ constexpr int lane_stride(int n, int w = 64) {
   // lanes) one 16-byte shared-memory wavefront (128 bytes: m = 8 slots)
   // serves W lanes x m/W positions; for W < m, lane offsets m/W apart modulo m
   // keep those accesses on distinct banks (1024-point fp64 strided passes:
-  // 8.9 -> 7.5 ms).  Odd offsets otherwise (and for fp32, where the residue
-  // rule measured slower).
+  // 8.9 -> 7.5 ms; 2048-point fp32 ones 0.82 -> 0.73 ms).  Odd offsets
+  // otherwise.
   constexpr int m = 128 / (int)sizeof(C);
   const int base = n + (n >> (sizeof(C) == 16 ? 3 : 4));
   if ((sizeof(C) != 16 && !DFFTB_LS_FP32) || w >= m) return base | 1;

@@ -90,10 +90,20 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
       : "memory");
 }
 
-template <typename T, int N, int W, int EXTRA = 0>
+// Staging rows of the per-thread cp.async loader for 8-byte-aligned fp32
+// rows (ADJ, W >= 16): W + 2 slots, so a row that starts 8 bytes off the
+// 16-byte grid lands one slot later and its inner lanes still move as 16-byte
+// pairs.
+template <typename T, bool ADJ, int W>
+struct RowPad {
+  static constexpr int value = (ADJ && sizeof(T) == 4 && W >= 16) ? 2 : 0;
+};
+
+template <typename T, int N, int W, int EXTRA = 0, int PADR = 0>
 struct TmaLayout {
   using C = Cpx<T>;
-  static constexpr int STG = W * (N + EXTRA) * (int)sizeof(C);  // one staging slot (EXTRA: C2Rh's bin N + pad)
+  // one staging slot (EXTRA: C2Rh's bin N + pad; PADR: cp.async row padding)
+  static constexpr int STG = (W + PADR) * (N + EXTRA) * (int)sizeof(C);
   static constexpr int XCH = W * lane_stride<C>(N, W) * (int)sizeof(C);
 };
 
@@ -343,7 +353,8 @@ __global__ void __launch_bounds__(W* Sched<N, EPREF>::TPL, MINB)
                         const TmaArgs ta) {
   using C = Cpx<T>;
   using SC = Sched<N, EPREF>;
-  using TL = TmaLayout<T, N, W, LK == kC2Rh ? kC2RhExtra : 0>;
+  constexpr int PADR = RowPad<T, ADJ, W>::value;
+  using TL = TmaLayout<T, N, W, LK == kC2Rh ? kC2RhExtra : 0, PADR>;
   constexpr int TPL = SC::TPL;
   constexpr int LS = lane_stride<C>(N, ADJ ? W : 64);
   extern __shared__ __align__(1024) unsigned char smem_tma[];
@@ -375,6 +386,46 @@ __global__ void __launch_bounds__(W* Sched<N, EPREF>::TPL, MINB)
     tile_coords(ta, t, alpha, beta0);
     beta0 *= W;
     unsigned char* dst = stg + s * TL::STG;
+    if constexpr (ADJ && PADR > 0) {
+      if (ta.ldgsts) {
+        // fp32 rows 8-byte aligned only (C2R user blocks of n/2+1 bins):
+        // 16-byte cp.async pairs of adjacent lanes.  Row i lands at slot
+        // i*(W+2) + par(i): an aligned row as W/2 pairs; a row 8 bytes off
+        // as lane 0 alone, W/2-1 pairs, lane W-1 alone (lanes in_sb = 1
+        // apart).  Lanes past B read as zero.
+        const C* src0 = reinterpret_cast<const C*>(p.in) + (int64_t)alpha * p.in_sa + beta0;
+        const int64_t par0 = (int64_t)(reinterpret_cast<uintptr_t>(src0) >> 3);
+        constexpr int RS = W + PADR, UPR = W / 2 + 1;  // slots and copy units per row
+        constexpr int NT = W * TPL;
+        const int nval = p.B - beta0;  // valid lanes of this tile
+        for (int e = tid; e < UPR * N; e += NT) {
+          const int i = e / UPR, u = e - (e / UPR) * UPR;
+          const int par = (int)((par0 + (int64_t)i * p.in_si) & 1);
+          int w0, cnt;  // first lane, lanes (1 or 2)
+          if (!par) {
+            if (u == UPR - 1) continue;
+            w0 = 2 * u;
+            cnt = 2;
+          } else {
+            w0 = u == 0 ? 0 : 2 * u - 1;
+            cnt = (u == 0 || u == UPR - 1) ? 1 : 2;
+          }
+          const int nv = min(max(nval - w0, 0), cnt);  // valid lanes of this unit
+          // the unit's own (16-byte aligned for pairs) address even when
+          // nv < cnt: only 8*nv bytes are read
+          const C* src = src0 + (int64_t)i * p.in_si + w0;
+          const uint32_t sdst = smem_u32(dst + ((size_t)i * RS + w0 + par) * sizeof(C));
+          if (cnt == 2)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sdst), "l"(src), "r"(8 * nv)
+                         : "memory");
+          else
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(sdst), "l"(src), "r"(8 * nv)
+                         : "memory");
+        }
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&bars[s])) : "memory");
+        return;
+      }
+    }
     if (ADJ && ta.ldgsts) {
       // very large row strides (e.g. the axis-0 pass) translate one page per
       // row: spread the rows over all threads' LSU path instead of one TMA
@@ -441,7 +492,20 @@ __global__ void __launch_bounds__(W* Sched<N, EPREF>::TPL, MINB)
     beta = beta * W + w;
     const unsigned char* st = stg + s * TL::STG;
     C v[SC::E];
-    if constexpr (ADJ) {
+    if constexpr (ADJ && PADR > 0) {
+      const C* scp = reinterpret_cast<const C*>(st);
+      if (ta.ldgsts) {
+        // padded rows of the paired cp.async loader (see issue)
+        const int64_t par0 = (int64_t)(reinterpret_cast<uintptr_t>(reinterpret_cast<const C*>(p.in) +
+                                                                   (int64_t)alpha * p.in_sa + (beta - w)) >> 3);
+        fetch0_lk<T, N, EPREF, LK>(
+            v, j, [&](int pos) { return scp[pos * (W + PADR) + w + (int)((par0 + (int64_t)pos * p.in_si) & 1)]; },
+            [&](int) { return T(0); });
+      } else {
+        fetch0_lk<T, N, EPREF, LK>(
+            v, j, [&](int pos) { return scp[pos * W + w]; }, [&](int) { return T(0); });
+      }
+    } else if constexpr (ADJ) {
       const C* scp = reinterpret_cast<const C*>(st);
       fetch0_lk<T, N, EPREF, LK>(
           v, j, [&](int pos) { return scp[pos * W + w]; }, [&](int) { return T(0); });

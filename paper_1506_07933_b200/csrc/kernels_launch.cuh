@@ -76,7 +76,7 @@ static cudaError_t launch_prec(int n, const PassParams& p, bool adj, cudaStream_
 }
 
 // TMA variant: one persistent CTA per SM, 512 threads, STAGES-deep prefetch
-template <typename T, int N, int EXTRA = 0, bool HALFREAL = false>
+template <typename T, int N, int EXTRA = 0, bool HALFREAL = false, bool ADJ = false>
 struct TmaCfg {
   // fp32 long lanes use 16 elements per thread (radix-16 stages): half the
   // threads per lane, so twice the adjacent lanes per CTA and 64-128 byte
@@ -107,14 +107,14 @@ struct TmaCfg {
   static constexpr int W = W0 < 1 ? 1 : (W0 > 64 ? 64 : W0);
   static constexpr int THREADS = W * TPL;
   static constexpr int MINB = DFFTB_TMA_MINB;
-  using TL = TmaLayout<T, N, W, EXTRA>;
+  using TL = TmaLayout<T, N, W, EXTRA, RowPad<T, ADJ, W>::value>;
   static constexpr int STAGES = (2 * TL::STG + TL::XCH + 128 <= (220 * 1024) / MINB) ? 2 : 1;
   static constexpr int SMEM = STAGES * TL::STG + TL::XCH + 8 * STAGES + 8 * kMaxDest;
 };
 
 template <typename T, int N, bool ADJ, int LK, bool SPEC = false>
 static cudaError_t launch_tma_tn(const PassParams& p, const TmaPlan& tp, int grid_limit, cudaStream_t s) {
-  using Cf = TmaCfg<T, N, LK == kC2Rh ? kC2RhExtra : 0, LK == kR2Ch || LK == kC2Rh>;
+  using Cf = TmaCfg<T, N, LK == kC2Rh ? kC2RhExtra : 0, LK == kR2Ch || LK == kC2Rh, ADJ>;
   auto kern = fft_pass_tma_kernel<T, N, Cf::EPREF, Cf::W, ADJ, Cf::STAGES, LK, SPEC, Cf::MINB>;
   static int occ_of[64] = {0}, sms_of[64] = {0};
   int dev = 0;

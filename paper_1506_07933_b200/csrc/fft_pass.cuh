@@ -306,6 +306,34 @@ __host__ __device__ constexpr int lane_stride(int n, int w = 64) {
   return base + ((r - base % m) % m + m) % m;
 }
 
+// Lanes as rows (contiguous lanes, lane-major threads): a warp spans 32/TPL
+// lanes of TPL threads; when a lane's TPL slots fill less than a wavefront
+// (m slots), a stride of TPL modulo m puts the lanes of a warp side by side
+// in the exchange buffer instead of on the same banks (half-length
+// 128-point fp32 lanes, 8 threads per lane: R2C pass 0.553 -> 0.488 ms, C2R
+// 0.531 -> 0.506 ms; profiles/r2/ab_lanestride_rows_s51.txt).
+#ifndef DFFTB_LS_ROWS
+#define DFFTB_LS_ROWS 1
+#endif
+template <typename C>
+__host__ __device__ constexpr int lane_stride_rows(int n, int tpl) {
+  constexpr int m = 128 / (int)sizeof(C);
+  const int base = n + (n >> (sizeof(C) == 16 ? 3 : 4));
+  if (!DFFTB_LS_ROWS || tpl >= m || (m % tpl) != 0) return base | 1;
+  return base + ((tpl - base % m) % m + m) % m;
+}
+
+// lane stride of the exchange buffer of a TMA pass kernel
+template <typename T, int N, int EPREF, int W, bool ADJ>
+__host__ __device__ constexpr int pass_lane_stride() {
+  using C = Cpx<T>;
+  if constexpr (ADJ) {
+    return lane_stride<C>(N, W);
+  } else {
+    return lane_stride_rows<C>(N, Sched<N, EPREF>::TPL);
+  }
+}
+
 template <typename T>
 __device__ __forceinline__ unsigned long long dbits(T v) {
   return static_cast<unsigned long long>(__double_as_longlong(static_cast<double>(v)));

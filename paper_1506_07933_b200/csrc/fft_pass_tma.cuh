@@ -99,12 +99,13 @@ struct RowPad {
   static constexpr int value = (ADJ && sizeof(T) == 4 && W >= 16) ? 2 : 0;
 };
 
-template <typename T, int N, int W, int EXTRA = 0, int PADR = 0>
+template <typename T, int N, int W, int EXTRA = 0, int PADR = 0, int LSV = 0>
 struct TmaLayout {
   using C = Cpx<T>;
   // one staging slot (EXTRA: C2Rh's bin N + pad; PADR: cp.async row padding)
   static constexpr int STG = (W + PADR) * (N + EXTRA) * (int)sizeof(C);
-  static constexpr int XCH = W * lane_stride<C>(N, W) * (int)sizeof(C);
+  // exchange buffer: W lanes of LSV slots (the kernel's lane stride)
+  static constexpr int XCH = W * (LSV > 0 ? LSV : lane_stride<C>(N, W)) * (int)sizeof(C);
 };
 
 // stage-0 fetch from a staging slot, compile-time lane kind
@@ -354,9 +355,9 @@ __global__ void __launch_bounds__(W* Sched<N, EPREF>::TPL, MINB)
   using C = Cpx<T>;
   using SC = Sched<N, EPREF>;
   constexpr int PADR = RowPad<T, ADJ, W>::value;
-  using TL = TmaLayout<T, N, W, LK == kC2Rh ? kC2RhExtra : 0, PADR>;
+  constexpr int LS = pass_lane_stride<T, N, EPREF, W, ADJ>();
+  using TL = TmaLayout<T, N, W, LK == kC2Rh ? kC2RhExtra : 0, PADR, LS>;
   constexpr int TPL = SC::TPL;
-  constexpr int LS = lane_stride<C>(N, ADJ ? W : 64);
   extern __shared__ __align__(1024) unsigned char smem_tma[];
   unsigned char* stg = smem_tma;
   C* xch = reinterpret_cast<C*>(smem_tma + STAGES * TL::STG);

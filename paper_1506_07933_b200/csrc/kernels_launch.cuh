@@ -107,7 +107,7 @@ struct TmaCfg {
   static constexpr int W = W0 < 1 ? 1 : (W0 > 64 ? 64 : W0);
   static constexpr int THREADS = W * TPL;
   static constexpr int MINB = DFFTB_TMA_MINB;
-  using TL = TmaLayout<T, N, W, EXTRA, RowPad<T, ADJ, W>::value>;
+  using TL = TmaLayout<T, N, W, EXTRA, RowPad<T, ADJ, W>::value, pass_lane_stride<T, N, EPREF, W, ADJ>()>;
   static constexpr int STAGES = (2 * TL::STG + TL::XCH + 128 <= (220 * 1024) / MINB) ? 2 : 1;
   static constexpr int SMEM = STAGES * TL::STG + TL::XCH + 8 * STAGES + 8 * kMaxDest;
 };

@@ -164,6 +164,16 @@ struct Ctx {
   std::vector<void*> events;  // cudaEvent_t pool, grown on demand
   // cached programs: key (plan id, buffers, parity, epilogue) -> program
   std::map<std::string, std::shared_ptr<Program>> programs;
+  // the two most recent plain executes (a forward / inverse pair alternates):
+  // found without formatting the map key
+  struct Recent {
+    uint64_t id = 0;
+    const void* in = nullptr;
+    const void* out = nullptr;
+    int parity = -1;
+    Program* pr = nullptr;
+  } recent[2];
+  int recent_next = 0;
   std::vector<uint64_t> checked_plans;  // plan ids whose buffer needs fit
   std::vector<OpTime> last_ops;
 

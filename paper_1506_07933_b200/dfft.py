@@ -517,23 +517,24 @@ def execute(plan: Plan, x: DistTensor, ctx: ExecContext,
     stream unless timers are requested or the plan needs its deferred checks
     (C2R Hermitian check, finiteness validation) — then errors surface here
     as in the reference."""
-    if x.dist != plan.input:
+    if x.dist is not plan.input and x.dist != plan.input:
         raise Error(17, "input layout differs from the plan's")
-    if x.data.device.type != "cuda":
+    dev = x.data.device
+    if dev.type != "cuda":
         raise Error(23, "DistTensor data must live on a CUDA device")
     if out is None:
         out = DistTensor(plan.output, x.rank,
                          torch.empty(plan.output.local_count(x.rank),
-                                     dtype=plan.dtype_of(plan.output), device=x.data.device))
+                                     dtype=plan.dtype_of(plan.output), device=dev))
     if sync is None:
         sync = _needs_sync(plan)
     xd = x.data if x.data.is_contiguous() else x.data.contiguous()
-    stream = torch.cuda.current_stream(x.data.device).cuda_stream
+    # the library switches to the context's device itself (and back)
+    stream = torch.cuda.current_stream(dev).cuda_stream
     tc = _lib.TimingC() if timers is not None else None
-    with torch.cuda.device(x.data.device):
-        _check(_lib.lib().dfftb_execute(plan._h, ctx._h, xd.data_ptr(), out.data.data_ptr(),
-                                        stream, 1 if sync else 0,
-                                        ctypes.byref(tc) if tc is not None else None))
+    _check(_lib.lib().dfftb_execute(plan._h, ctx._h, xd.data_ptr(), out.data.data_ptr(),
+                                    stream, 1 if sync else 0,
+                                    ctypes.byref(tc) if tc is not None else None))
     if timers is not None:
         for k in ("local_fft", "pack", "unpack", "staging_copy", "wire_comm", "total"):
             setattr(timers, k, getattr(timers, k) + getattr(tc, k))

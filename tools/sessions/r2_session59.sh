@@ -1,0 +1,17 @@
+#!/bin/bash
+# round-2 GPU session 59 (4 GPUs): final-code GPU suite, bench lines and configs at N=1/2/4 (after the lane-stride, program-cache and Python execute changes)
+O=gpurun_out/s59
+mkdir -p $O
+TR="python -m torch.distributed.run --nnodes=1 --master-addr 127.0.0.1"
+timeout 1800 python -m pytest tests -m gpu -q -s > $O/pytest_gpu.log 2>&1; echo "exit $?" >> $O/pytest_gpu.log
+tail -3 $O/pytest_gpu.log
+timeout 300 python bench.py > $O/bench_n1.log 2>&1
+timeout 300 $TR --nproc-per-node 2 --master-port 29671 bench.py --gpus 2 > $O/bench_n2.log 2>&1
+timeout 300 $TR --nproc-per-node 4 --master-port 29672 bench.py --gpus 4 > $O/bench_n4.log 2>&1
+timeout 300 python bench.py --impl reference --steps 2 --warmup 1 > $O/bench_ref.log 2>&1
+for f in $O/bench_n*.log; do echo "$f: $(grep -o '"ms_per_step": [0-9.]*' $f | head -1)"; done
+timeout 300 python tools/bench_configs.py > $O/configs_n1.log 2>&1
+timeout 400 $TR --nproc-per-node 2 --master-port 29673 tools/bench_configs.py > $O/configs_n2.log 2>&1
+timeout 400 $TR --nproc-per-node 4 --master-port 29674 tools/bench_configs.py > $O/configs_n4.log 2>&1
+grep -h '"config"' $O/configs_n*.log
+echo done

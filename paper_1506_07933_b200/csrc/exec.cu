@@ -402,7 +402,13 @@ Ctx* ctx_create(const Plan& plan, int rank, int device) {
   ctx->table_bytes = table_bytes(plan);
   CUDA_TRY(cudaMalloc(&ctx->region, ctx->region_bytes));
   ctx->staging_bytes = staging_bytes(plan, blk);
-  if (ctx->staging_bytes) CUDA_TRY(cudaMalloc(&ctx->staging, ctx->staging_bytes));
+  if (ctx->staging_bytes && cudaMalloc(&ctx->staging, ctx->staging_bytes) != cudaSuccess) {
+    // no room for staging images: this rank exchanges by direct peer stores,
+    // and ctx_connect makes every rank do the same (programs must agree)
+    cudaGetLastError();
+    ctx->staging = nullptr;
+    ctx->staging_bytes = 0;
+  }
   CUDA_TRY(cudaMemset(ctx->region, 0, kFlagsBytes));
   if (ctx->work_bytes) CUDA_TRY(cudaMalloc(&ctx->work, ctx->work_bytes));
   CUDA_TRY(cudaMalloc(&ctx->dstat, kStatWords * sizeof(unsigned long long)));
@@ -461,6 +467,7 @@ void ctx_export(const Ctx& ctx, CtxHandle* h) {
   h->dptr = (uint64_t)(uintptr_t)ctx.region;
   h->bytes = ctx.region_bytes;
   h->magic = kHandleMagic;
+  h->staged = ctx.staging != nullptr ? 1 : 0;
 }
 
 static void enable_peer(int dev, int peer) {
@@ -504,6 +511,15 @@ void ctx_connect(Ctx& ctx, const CtxHandle* handles) {
       ctx.peer_region[r] = p;
       ctx.peer_opened[r] = true;
     }
+  }
+  // the staged exchange changes the program structure: only if every rank has
+  // its staging images
+  bool all_staged = true;
+  for (int r = 0; r < ctx.nranks; ++r) all_staged = all_staged && handles[r].staged;
+  if (!all_staged && ctx.staging) {
+    cudaFree(ctx.staging);
+    ctx.staging = nullptr;
+    ctx.staging_bytes = 0;
   }
   ctx.connected = true;
 }

@@ -105,7 +105,8 @@ struct CtxHandle {
   uint64_t dptr;          // base pointer in the owning process
   uint64_t bytes;
   uint64_t magic;
-  unsigned char pad[24];
+  unsigned char staged;   // the owner allocated staging images (all ranks must agree)
+  unsigned char pad[23];
 };
 static_assert(sizeof(CtxHandle) == 128, "handle must stay 128 bytes");
 

@@ -1306,21 +1306,24 @@ static void overlap_pairs(std::vector<Op>& prog, const Plan& plan, const Ctx& ct
 
 // ---------------------------------------------------------- staged exchange
 //
-// ExchangePath::Staged on the copy engine (or every plan with DFFTB_DMA=1).  The same
-// [P: exchange pass][sync][Q: local pass] triple, in C chunks along the same
-// shared lane axis X as above, becomes
+// The default exchange of Blocking / Staged plans (DFFTB_DMA=0 turns it off;
+// Pipelined plans use overlap_pairs above), after the staging hop of
+// staged_all_to_all (exchange.hpp:225-246).  The same [P: exchange pass]
+// [sync][Q: local pass] triple, in C chunks along the same shared lane axis X
+// as above, becomes
 //   caller's stream: P chunk 0 .. C-1 on every SM, storing the other
 //     members' parts into local staging images of their buffers (same
-//     layout and offsets; pack_into_staging, exchange.hpp) and its own part
-//     into its own buffer -- HBM-speed stores only;  then per chunk c:
-//     wait for sync point k_c, Q chunk c on every SM;
-//   copy stream: per chunk c: wait for P chunk c, copy chunk c's box of
-//     every staging image into that member's buffer (one pitched 3-D DMA
-//     per member over NVLink), signal k_c to the group.
-// No SM ever stalls on NVLink: the copy engine streams chunk c while the SMs
+//     layout and offsets) and its own part into its own buffer -- HBM-speed
+//     stores only;  then per chunk c: wait for sync point k_c, Q chunk c on
+//     every SM;
+//   copy stream c % 2: wait for P chunk c, copy chunk c's box of every
+//     staging image into that member's buffer (one pitched 2-D DMA per member
+//     over NVLink), signal k_c to the group.
+// No SM ever stalls on NVLink: the copy engines stream chunk c while the SMs
 // run P's later chunks and Q's earlier ones.  The op and sync sequence is
-// rank-independent (C signals and C waits per triple); chunk ranges are
-// multiples of 64 lanes along a tile axis, which every tile width divides.
+// rank-independent (C signals and C waits per triple, staged or not decided
+// from global sizes); chunk ranges are multiples of 64 lanes along a tile
+// axis, which every tile width divides.
 
 // staging images: one buffer per other member of the largest exchange group
 static size_t staging_bytes(const Plan& plan, size_t blk) {

@@ -79,6 +79,7 @@ struct Knobs {
   bool rhalf = true;          // DFFTB_RHALF: R2C / C2R lanes as half-length complex FFTs
   int row_align = 32;         // DFFTB_ROW_ALIGN: internal row padding in bytes (16, 32 or 64)
   bool dma_flat = true;       // DFFTB_DMA_FLAT: staged exchanges keep the [x0][x1][x2] order (2-D boxes)
+  int dma_max_group = 2;      // DFFTB_DMA_MAX_GROUP: stage exchanges of at most this many members
   int dma_streams = 2;        // DFFTB_DMA_STREAMS: copy streams of the staged exchange (1..4; chunks
                               // round-robin, so up to that many DMAs in flight)
   bool r2c_order = true;      // DFFTB_R2C_ORDER: single-rank R2C forward as F2, F0, F1
@@ -114,6 +115,7 @@ static const Knobs& knobs() {
     if (const char* e = getenv("DFFTB_DMA_MIN_MB")) k.dma_min_mb = atof(e);
     if (const char* e = getenv("DFFTB_DMA_MIN_ROW")) k.dma_min_row = atoi(e);
     k.dma_flat = flag("DFFTB_DMA_FLAT", true);
+    if (const char* e = getenv("DFFTB_DMA_MAX_GROUP")) k.dma_max_group = atoi(e);
     if (const char* e = getenv("DFFTB_DMA_STREAMS")) k.dma_streams = std::max(1, std::min(kCopyStreams, atoi(e)));
     if (const char* e = getenv("DFFTB_ROW_ALIGN")) {
       const int a = atoi(e);
@@ -1401,7 +1403,12 @@ static void staged_pairs(std::vector<Op>& prog, const Plan& plan, const Ctx& ctx
       const bool x_inner = X == B.ndim() - 1;  // receiver rows are X-chunks
       const int64_t u = (X == prog[i].ax_b || X == prog[i + 2].ax_b) ? 64 : 1;
       const int64_t Rg = ((Xg + C - 1) / C + u - 1) / u * u;
-      pattern = per_rank >= knobs().dma_min_mb * 1048576.0 && (!x_inner || Rg * csize >= knobs().dma_min_row);
+      // groups of more than two: direct peer stores reach several peers at
+      // once and win (512^3 on 4 GPUs, slab 4 / pencil 1x4: 1.95 direct vs
+      // 2.5-2.6 ms staged, profiles/r2/group_probe_s76.txt)
+      const bool small_group = (int)prog[i].members.size() <= knobs().dma_max_group;
+      pattern = small_group && per_rank >= knobs().dma_min_mb * 1048576.0 &&
+                (!x_inner || Rg * csize >= knobs().dma_min_row);
     }
     if (!pattern) {
       out.push_back(prog[i++]);

@@ -23,7 +23,8 @@ def _ngpus():
 # default: the shipped thresholds (these small cases exchange by direct peer
 # stores); staged: every eligible exchange goes through staging images and
 # copy-engine DMAs (size thresholds off), checked to have run
-MODES = {"default": {}, "staged": {"DFFTB_DMA_MIN_MB": "0", "DFFTB_DMA_MIN_ROW": "0", "DFFTB_EXPECT_STAGED": "1"}}
+MODES = {"default": {}, "staged": {"DFFTB_DMA_MIN_MB": "0", "DFFTB_DMA_MIN_ROW": "0", "DFFTB_DMA_MAX_GROUP": "64",
+                               "DFFTB_EXPECT_STAGED": "1"}}
 
 
 @pytest.mark.parametrize("mode", list(MODES))
